@@ -1,0 +1,342 @@
+// CPU ORACLE (test infrastructure only): C-ABI used by tests/ (ctypes) and
+// by bench.py's cpu_baseline / --impl reference leg. Never used by the product.
+#include <cstring>
+#include <mutex>
+#include <thread>
+
+#include "oracle.hpp"
+
+using namespace oracle;
+
+namespace {
+thread_local std::string g_err;
+std::mutex g_mu;
+std::vector<std::unique_ptr<Scenario>> g_sc;
+std::vector<std::shared_ptr<const LinearizedTrajectory>> g_tr;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return -22;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -34;
+  }
+}
+Scenario& sc(int h) {
+  std::lock_guard<std::mutex> l(g_mu);
+  if (h < 0 || h >= static_cast<int>(g_sc.size()) || !g_sc[h]) throw std::invalid_argument("bad scenario handle");
+  return *g_sc[h];
+}
+std::shared_ptr<const LinearizedTrajectory> tr(int h) {
+  std::lock_guard<std::mutex> l(g_mu);
+  if (h < 0 || h >= static_cast<int>(g_tr.size()) || !g_tr[h]) throw std::invalid_argument("bad trajectory handle");
+  return g_tr[h];
+}
+Vec vin(const double* p, int64_t n) { return Vec(p, p + n); }
+void vout(const Vec& v, double* p) { std::memcpy(p, v.data(), v.size() * sizeof(double)); }
+Mat min_(const double* p, int64_t r, int64_t c) {
+  Mat m(r, c);
+  std::memcpy(m.a.data(), p, sizeof(double) * r * c);
+  return m;
+}
+SketchMethod meth(int m) {
+  switch (m) {
+    case 0: return SketchMethod::RandSVD;
+    case 1: return SketchMethod::Nystrom;
+    case 2: return SketchMethod::SingleView;
+    case 3: return SketchMethod::Lanczos;
+  }
+  throw std::invalid_argument("unknown sketch method");
+}
+}  // namespace
+
+extern "C" {
+
+const char* oracle_last_error() { return g_err.c_str(); }
+uint64_t oracle_mix_seed(uint64_t s, uint64_t t) { return mix_seed(s, t); }
+int oracle_hardware_threads() { return static_cast<int>(std::thread::hardware_concurrency()); }
+
+int oracle_gaussian_matrix(int64_t n, int64_t l, uint64_t seed, double* out) {
+  return guard([&] { vout(gaussian_matrix(n, l, seed).a, out); });
+}
+
+// cfg 0..4 = BASELINE configs, 100 = burgers_1_1 preset.
+int oracle_scenario_create(int cfg) {
+  int h = -1;
+  const int rc = guard([&] {
+    auto s = std::make_unique<Scenario>(cfg == 100 ? make_reference_burgers_1_1() : make_config(cfg));
+    std::lock_guard<std::mutex> l(g_mu);
+    g_sc.push_back(std::move(s));
+    h = static_cast<int>(g_sc.size()) - 1;
+  });
+  return rc == 0 ? h : rc;
+}
+void oracle_scenario_destroy(int h) {
+  std::lock_guard<std::mutex> l(g_mu);
+  if (h >= 0 && h < static_cast<int>(g_sc.size())) g_sc[h].reset();
+}
+// info: [dim, n_obs, n_t, spi]
+int oracle_scenario_info(int h, int64_t* info) {
+  return guard([&] {
+    const auto& p = sc(h).problem;
+    info[0] = p.state_dim();
+    info[1] = p.n_obs();
+    info[2] = p.n_t;
+    info[3] = p.steps_per_interval;
+  });
+}
+int oracle_scenario_arrays(int h, double* background, double* truth0, int64_t* indices, double* values,
+                           double* variances) {
+  return guard([&] {
+    const auto& s = sc(h);
+    const auto& p = s.problem;
+    if (background) vout(p.background, background);
+    if (truth0) vout(s.truth0, truth0);
+    if (indices) std::memcpy(indices, p.obs.indices.data(), sizeof(int64_t) * p.obs.indices.size());
+    if (values) vout(p.obs.values.a, values);
+    if (variances) vout(p.obs.variances.a, variances);
+  });
+}
+int oracle_prior_sqrt(int h, const double* v, double* out) {
+  return guard([&] {
+    const auto& p = sc(h).problem;
+    vout(p.prior->apply_sqrt(vin(v, p.state_dim())), out);
+  });
+}
+int oracle_forward(int h, const double* x0, int steps, double* out) {
+  return guard([&] {
+    const auto& p = sc(h).problem;
+    vout(p.model->forward(vin(x0, p.state_dim()), steps), out);
+  });
+}
+int oracle_linearize(int h, const double* x0) {
+  int th = -1;
+  const int rc = guard([&] {
+    const auto& p = sc(h).problem;
+    auto t = p.model->linearize(vin(x0, p.state_dim()), p.total_steps(), p.steps_per_interval);
+    std::lock_guard<std::mutex> l(g_mu);
+    g_tr.push_back(std::move(t));
+    th = static_cast<int>(g_tr.size()) - 1;
+  });
+  return rc == 0 ? th : rc;
+}
+void oracle_traj_destroy(int t) {
+  std::lock_guard<std::mutex> l(g_mu);
+  if (t >= 0 && t < static_cast<int>(g_tr.size())) g_tr[t].reset();
+}
+int oracle_tlm_range(int h, int t, int b, int e, const double* dx, double* out) {
+  return guard([&] { vout(tr(t)->tlm_range(b, e, vin(dx, sc(h).problem.state_dim())), out); });
+}
+int oracle_adj_range(int h, int t, int b, int e, const double* lam, double* out) {
+  return guard([&] { vout(tr(t)->adj_range(b, e, vin(lam, sc(h).problem.state_dim())), out); });
+}
+int oracle_state_at(int h, int t, int step, double* out) {
+  return guard([&] {
+    (void)sc(h);
+    vout(tr(t)->state_at(step), out);
+  });
+}
+// Block misfit: V n x s -> Y m x s (column-major), threads over columns.
+int oracle_misfit_apply_block(int h, int t, const double* v, int s, double* y, int workers) {
+  return guard([&] {
+    const auto& p = sc(h).problem;
+    const MisfitOperator op(p, tr(t));
+    vout(apply_columns(op, min_(v, p.state_dim(), s), false, workers).a, y);
+  });
+}
+int oracle_misfit_adjoint_block(int h, int t, const double* w, int s, double* z, int workers) {
+  return guard([&] {
+    const auto& p = sc(h).problem;
+    const MisfitOperator op(p, tr(t));
+    vout(apply_columns(op, min_(w, p.misfit_dim(), s), true, workers).a, z);
+  });
+}
+int oracle_gram_block(int h, int t, const double* v, int s, double* hv, int workers) {
+  return guard([&] {
+    const auto& p = sc(h).problem;
+    const MisfitOperator op(p, tr(t));
+    const GramMap g(op);
+    vout(apply_columns(g, min_(v, p.state_dim(), s), false, workers).a, hv);
+  });
+}
+// out: cost; ctrl_grad (n); lambda0 (n); innovations (m). z may be null for x-space priors.
+int oracle_evaluate(int h, const double* x0, const double* z, double* cost, double* ctrl_grad, double* lambda0,
+                    double* innov) {
+  return guard([&] {
+    const auto& p = sc(h).problem;
+    Vec zz;
+    if (z) zz = vin(z, p.state_dim());
+    const Evaluation ev = evaluate(p, vin(x0, p.state_dim()), z ? &zz : nullptr, nullptr);
+    *cost = ev.cost;
+    if (ctrl_grad) vout(ev.ctrl_gradient, ctrl_grad);
+    if (lambda0) vout(ev.lambda0, lambda0);
+    if (innov) vout(ev.innovations, innov);
+  });
+}
+// Sketch of the misfit Hessian at trajectory t. method 0..3. Outputs: eig (rank),
+// basis (n x rank); counts[0..2] = tlm, adj, final_rank.
+int oracle_sketch(int h, int t, int method, int rank, int rank2, uint64_t seed, int workers, double* eig,
+                  double* basis, int64_t* counts) {
+  return guard([&] {
+    const auto& p = sc(h).problem;
+    const MisfitOperator op(p, tr(t));
+    const GramMap hop(op);
+    SketchReport r;
+    switch (meth(method)) {
+      case SketchMethod::RandSVD: r = randsvd_sketch(op, rank, seed, workers); break;
+      case SketchMethod::Nystrom: r = nystrom_sketch(hop, rank, seed, workers); break;
+      case SketchMethod::SingleView:
+        r = singleview_sketch(op, rank, rank2 > 0 ? rank2 : 2 * rank + 1, seed, workers);
+        break;
+      case SketchMethod::Lanczos: {
+        Vec st = gaussian_vector(p.state_dim(), seed);
+        r = lanczos_sketch(hop, rank, st);
+        break;
+      }
+    }
+    vout(r.evd.eigenvalues, eig);
+    if (basis) vout(r.evd.basis.a, basis);
+    counts[0] = r.tlm_applies;
+    counts[1] = r.adj_applies;
+    counts[2] = r.final_rank;
+  });
+}
+// GN solve. params: [mode, method, rank, rank2, growth, max_rank, max_gn_iters, pcg_max_iter, workers]
+// dparams: [grad_tol, pcg_tol, eps_sketch, eps_reuse]; negative/zero entries keep scenario defaults.
+// log: per iteration 16 doubles: k, cost, gnorm, step, pcg_iters, ls_trials, pcg_conv, recomputed,
+// final_rank, kappa_sk, kappa_re, fwd, tlm, adj, off_tlm, off_adj. eig0: first sketch eigenvalues.
+int oracle_gn_solve(int h, const int64_t* params, const double* dparams, uint64_t seed, double* analysis,
+                    double* log, int max_log, int* n_iters, double* summary, double* eig0, int max_eig) {
+  return guard([&] {
+    const Scenario& s = sc(h);
+    GNConfig g = s.gn;
+    if (params[0] >= 0) g.mode = static_cast<SolveMode>(params[0]);
+    if (params[1] >= 0) g.sketch.method = meth(static_cast<int>(params[1]));
+    if (params[2] > 0) g.sketch.rank = static_cast<int>(params[2]);
+    if (params[3] > 0) g.sketch.rank2 = static_cast<int>(params[3]);
+    if (params[4] > 0) g.sketch.growth = static_cast<int>(params[4]);
+    if (params[5] > 0) g.sketch.max_rank = static_cast<int>(params[5]);
+    if (params[6] > 0) g.max_gn_iters = static_cast<int>(params[6]);
+    if (params[7] > 0) g.pcg_max_iter = static_cast<int>(params[7]);
+    if (params[8] > 0) g.sketch.workers = static_cast<int>(params[8]);
+    if (dparams[0] > 0) g.grad_tol = dparams[0];
+    if (dparams[1] > 0) g.pcg_tol = dparams[1];
+    if (dparams[2] > 0) g.sketch.eps_sketch = dparams[2];
+    if (dparams[3] > 0) g.sketch.eps_reuse = dparams[3];
+    if (seed != ~0ULL) g.sketch.seed = seed;
+    const GNResult r = gn_solve(s.problem, g);
+    vout(r.analysis, analysis);
+    *n_iters = static_cast<int>(r.iterations.size());
+    for (size_t i = 0; i < r.iterations.size() && static_cast<int>(i) < max_log; ++i) {
+      const auto& L = r.iterations[i];
+      double* o = log + 16 * i;
+      o[0] = L.k;
+      o[1] = L.cost;
+      o[2] = L.grad_inf_norm;
+      o[3] = L.step_size;
+      o[4] = L.pcg_iterations;
+      o[5] = L.line_search_trials;
+      o[6] = L.pcg_converged;
+      o[7] = L.sketch_recomputed;
+      o[8] = L.final_rank;
+      o[9] = L.kappa_sk;
+      o[10] = L.kappa_re;
+      o[11] = L.totals.fwd;
+      o[12] = L.totals.tlm;
+      o[13] = L.totals.adj;
+      o[14] = L.totals.offline_tlm;
+      o[15] = L.totals.offline_adj;
+    }
+    summary[0] = r.final_cost;
+    summary[1] = r.final_grad_inf_norm;
+    summary[2] = static_cast<double>(r.total_pcg);
+    summary[3] = r.converged;
+    summary[4] = r.line_search_failed;
+    if (eig0 && !r.iterations.empty()) {
+      const auto& e = r.iterations[0].eigenvalues;
+      for (int i = 0; i < max_eig; ++i) eig0[i] = i < static_cast<int>(e.size()) ? e[i] : NAN;
+    }
+  });
+}
+
+// ---- dense helpers for unit tests ----
+int oracle_thin_qr(int64_t n, int64_t l, const double* y, double* q, double* r, int64_t* ndef) {
+  return guard([&] {
+    const ThinQR t = thin_qr(min_(y, n, l));
+    vout(t.q.a, q);
+    vout(t.r.a, r);
+    *ndef = static_cast<int64_t>(t.deficient_columns.size());
+  });
+}
+int oracle_thin_svd(int64_t r, int64_t c, const double* a, double* u, double* s, double* v) {
+  return guard([&] {
+    const ThinSVD t = thin_svd(min_(a, r, c));
+    vout(t.u.a, u);
+    vout(t.s, s);
+    vout(t.v.a, v);
+  });
+}
+int oracle_woodbury(int64_t n, int64_t l, const double* basis, const double* lam, const double* v, double* out) {
+  return guard([&] {
+    LowRankEVD e{min_(basis, n, l), vin(lam, l)};
+    vout(woodbury_apply(e, vin(v, n)), out);
+  });
+}
+// PCG on a dense SPD matrix; precond: 0 none, 1 exact inverse given in minv.
+int oracle_pcg_dense(int64_t n, const double* a, const double* rhs, const double* minv, double tol, int max_iter,
+                     double* x, int* iters, int* converged) {
+  return guard([&] {
+    const DenseMap op(min_(a, n, n));
+    Preconditioner pre;
+    Mat mi;
+    if (minv) {
+      mi = min_(minv, n, n);
+      pre = [&mi](const Vec& r) { return matvec(mi, r); };
+    }
+    const PCGReport rep = pcg_solve(op, vin(rhs, n), pre, tol, max_iter);
+    vout(rep.solution, x);
+    *iters = rep.iterations;
+    *converged = rep.converged;
+  });
+}
+// Sketch of a dense symmetric PSD H = A^T A given A (m x n).
+int oracle_sketch_dense(int64_t m, int64_t n, const double* a, int method, int rank, int rank2, uint64_t seed,
+                        double* eig, double* basis) {
+  return guard([&] {
+    const DenseMap op(min_(a, m, n));
+    const GramMap hop(op);
+    SketchReport r;
+    switch (meth(method)) {
+      case SketchMethod::RandSVD: r = randsvd_sketch(op, rank, seed); break;
+      case SketchMethod::Nystrom: r = nystrom_sketch(hop, rank, seed); break;
+      case SketchMethod::SingleView: r = singleview_sketch(op, rank, rank2 > 0 ? rank2 : 2 * rank + 1, seed); break;
+      case SketchMethod::Lanczos: r = lanczos_sketch(hop, rank, gaussian_vector(n, seed)); break;
+    }
+    vout(r.evd.eigenvalues, eig);
+    vout(r.evd.basis.a, basis);
+  });
+}
+int oracle_bve_fixture(int nx, int ny, double re, double ro, double dt, int steps, uint64_t seed, double* out) {
+  return guard([&] { vout(bve_truth_fixture_regen(nx, ny, re, ro, dt, steps, seed), out); });
+}
+// Periodic BVE building blocks (n x n): op 0 poisson, 1 laplacian, 2 arakawa(a,b), 3 rhs.
+int oracle_bve_op(int n, int op, const double* a, const double* b, double* out) {
+  return guard([&] {
+    const PeriodicBVE m(n, 1e-4, 1e-3);
+    const int64_t d = m.dim();
+    switch (op) {
+      case 0: vout(m.poisson(vin(a, d)), out); break;
+      case 1: vout(m.laplacian(vin(a, d)), out); break;
+      case 2: vout(m.arakawa(vin(a, d), vin(b, d)), out); break;
+      case 3: vout(m.rhs(vin(a, d)), out); break;
+      default: throw std::invalid_argument("bad op");
+    }
+  });
+}
+
+}  // extern "C"
