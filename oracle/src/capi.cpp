@@ -65,17 +65,18 @@ int oracle_gaussian_matrix(int64_t n, int64_t l, uint64_t seed, double* out) {
   return guard([&] { vout(gaussian_matrix(n, l, seed).a, out); });
 }
 
-// cfg 0..4 = BASELINE configs, 100 = burgers_1_1 preset.
-int oracle_scenario_create(int cfg) {
+// cfg 0..4 = BASELINE configs (steps > 0 truncates the window), 100 = burgers_1_1 preset.
+int oracle_scenario_create_ex(int cfg, int steps, int spi) {
   int h = -1;
   const int rc = guard([&] {
-    auto s = std::make_unique<Scenario>(cfg == 100 ? make_reference_burgers_1_1() : make_config(cfg));
+    auto s = std::make_unique<Scenario>(cfg == 100 ? make_reference_burgers_1_1() : make_config(cfg, steps, spi));
     std::lock_guard<std::mutex> l(g_mu);
     g_sc.push_back(std::move(s));
     h = static_cast<int>(g_sc.size()) - 1;
   });
   return rc == 0 ? h : rc;
 }
+int oracle_scenario_create(int cfg) { return oracle_scenario_create_ex(cfg, -1, -1); }
 void oracle_scenario_destroy(int h) {
   std::lock_guard<std::mutex> l(g_mu);
   if (h >= 0 && h < static_cast<int>(g_sc.size())) g_sc[h].reset();

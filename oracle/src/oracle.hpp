@@ -510,7 +510,7 @@ struct Scenario {
   std::string name;
 };
 // cfg_id 0..4 = BASELINE.json configs; extra ids for reference presets.
-Scenario make_config(int cfg_id);
+Scenario make_config(int cfg_id, int steps_override = -1, int spi_override = -1);
 Scenario make_reference_burgers_1_1();  // preset burgers_1_1 (Dirichlet RK3)
 Vec bve_truth_fixture_regen(int nx, int ny, double re, double ro, double dt, int steps,
                             uint64_t seed);

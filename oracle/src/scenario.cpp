@@ -75,9 +75,14 @@ Vec periodic_grf_truth(int n, uint64_t seed) {
   return o;
 }
 
-Scenario make_config(int id) {
+Scenario make_config(int id, int steps_override, int spi_override) {
   if (id < 0 || id > 4) throw std::invalid_argument("make_config: config id must be 0..4");
-  const CfgSpec& c = kSpecs[id];
+  CfgSpec c = kSpecs[id];
+  if (spi_override > 0) c.spi = spi_override;
+  if (steps_override > 0) {
+    if (steps_override % c.spi) throw std::invalid_argument("make_config: steps must be a multiple of spi");
+    c.steps = steps_override;
+  }
   Scenario sc;
   sc.name = "config" + std::to_string(id);
   AssimilationProblem& p = sc.problem;

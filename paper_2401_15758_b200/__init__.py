@@ -1,0 +1,12 @@
+"""B200-native SC-4DVAR Gauss-Newton Hessian-product engine (arXiv 2401.15758 hot path).
+
+The compute path is ``_build/libsdv_cuda.so`` (hand-written sm_100a CUDA,
+C-ABI in ``include/sdv.h``); this package is its Python host mirror.
+"""
+from .api import (LANCZOS, MODEL_BURGERS, MODEL_BVE, NYSTROM, RANDSVD, SINGLEVIEW, DeviceBuffer, PinnedBuffer,
+                  Problem, Trajectory, gaussian_matrix, gaussian_vector, init, launch_count, mix_seed)
+from ._lib import LIB_PATH, SdvCudaError, SdvError
+
+__all__ = ["Problem", "Trajectory", "DeviceBuffer", "PinnedBuffer", "init", "launch_count", "mix_seed",
+           "gaussian_matrix", "gaussian_vector", "MODEL_BURGERS", "MODEL_BVE", "RANDSVD", "NYSTROM", "SINGLEVIEW",
+           "LANCZOS", "SdvError", "SdvCudaError", "LIB_PATH"]

@@ -1,0 +1,283 @@
+"""Python host mirror of the reference's hot-path interfaces over the C-ABI.
+
+Names and argument meaning follow /root/reference/proj/include/sketchdav:
+  Problem            <- AssimilationProblem + DynamicalModel + PriorCovariance
+  Problem.linearize  <- DynamicalModel::linearize          (model.hpp:36-40)
+  Trajectory         <- LinearizedTrajectory (state_at, tlm_range, adj_range)
+  MisfitOperator     <- MisfitOperator::apply/adjoint_apply (fourdvar.hpp:75-89)
+                        batched over column blocks (apply_columns, sketch.hpp:54-58)
+  Problem.evaluate   <- evaluate                            (fourdvar.cpp:92-132)
+  woodbury_apply, pcg_solve, sketches, gn_solve             (linalg/sketch/fourdvar)
+Errors map to ValueError (std::invalid_argument) and SdvError (std::runtime_error).
+Blocks are numpy arrays of shape (s, n) (row-major == column-major n x s).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import D, GNConfigC, I32, I64, ProblemDesc, check, lib
+
+MODEL_BURGERS, MODEL_BVE = 1, 2
+RANDSVD, NYSTROM, SINGLEVIEW, LANCZOS = 0, 1, 2, 3
+MODES = {"SketchSolv": 0, "SketchPrec": 1, "SketchPrecA": 2, "PrecGamma": 3, "PrecLanczos": 4, "PrecALanczos": 5}
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(D)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def init(device=0):
+    check(lib().sdv_device_init(device))
+
+
+def launch_count():
+    return int(lib().sdv_launch_count())
+
+
+def mix_seed(seed, stream):
+    return int(lib().sdv_mix_seed(seed, stream))
+
+
+def gaussian_matrix(n, l, seed):
+    """n x l standard normal block as an (l, n) array (column-major n x l)."""
+    out = np.empty((l, n))
+    check(lib().sdv_gaussian_matrix(n, l, seed, _p(out)))
+    return out
+
+
+def gaussian_vector(n, seed):
+    return gaussian_matrix(n, 1, seed)[0]
+
+
+class Problem:
+    """Device-resident AssimilationProblem for the periodic Burgers / BVE configs."""
+
+    def __init__(self, model, n, nu, dt, n_t, steps_per_interval, prior_sigma, prior_length, obs_indices, obs_values,
+                 obs_variances, background, block_group=0):
+        self.desc = ProblemDesc(model, n, nu, dt, n_t, steps_per_interval, prior_sigma, prior_length, block_group)
+        idx = np.ascontiguousarray(obs_indices, dtype=np.int64)
+        vals = _f64(obs_values)
+        var = _f64(obs_variances)
+        bg = _f64(background)
+        self._h = C.c_void_p()
+        check(lib().sdv_problem_create(C.byref(self.desc), idx.size, idx.ctypes.data_as(I64), _p(vals), _p(var),
+                                       _p(bg), C.byref(self._h)))
+        dims = np.zeros(6, np.int64)
+        check(lib().sdv_problem_dims(self._h, dims.ctypes.data_as(I64)))
+        self.n, self.m, self.n_obs, self.n_t, self.spi, self.total_steps = (int(x) for x in dims)
+        self.background = bg.copy()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            lib().sdv_problem_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def forward(self, x0, steps):
+        out = np.empty(self.n)
+        check(lib().sdv_forward(self._h, _p(_f64(x0)), steps, _p(out)))
+        return out
+
+    def linearize(self, x0):
+        t = C.c_void_p()
+        check(lib().sdv_linearize(self._h, _p(_f64(x0)), C.byref(t)))
+        return Trajectory(self, t)
+
+    def linearize_dev(self, x0_dev):
+        t = C.c_void_p()
+        check(lib().sdv_linearize_dev(self._h, C.c_void_p(x0_dev), C.byref(t)))
+        return Trajectory(self, t)
+
+    def prior_sqrt(self, V):
+        V = _f64(np.atleast_2d(V))
+        out = np.empty_like(V)
+        check(lib().sdv_prior_sqrt_block(self._h, _p(V), V.shape[0], _p(out)))
+        return out
+
+    def evaluate(self, x0, z=None):
+        """(cost, ctrl_grad, lambda0) in the control-variable form."""
+        cost = C.c_double()
+        g = np.empty(self.n)
+        lam = np.empty(self.n)
+        check(lib().sdv_evaluate(self._h, _p(_f64(x0)), _p(None if z is None else _f64(z)), C.byref(cost), _p(g),
+                                 _p(lam)))
+        return cost.value, g, lam
+
+    def woodbury_apply(self, basis, eig, V):
+        """basis: (l, n) rows = basis vectors; V: (s, n)."""
+        basis = _f64(np.atleast_2d(basis))
+        V = _f64(np.atleast_2d(V))
+        out = np.empty_like(V)
+        check(lib().sdv_woodbury_apply(self._h, basis.shape[0], _p(basis), _p(_f64(eig)), _p(V), V.shape[0],
+                                       _p(out)))
+        return out
+
+    def thin_qr(self, Y):
+        """Device Householder QR of an (n, l) matrix. Returns q (n, l), r (l, l), n_deficient."""
+        n, l = Y.shape
+        yt = _f64(np.asarray(Y).T)
+        q = np.empty((l, n))
+        r = np.empty((l, l))
+        nd = C.c_int()
+        check(lib().sdv_thin_qr(self._h, n, l, _p(yt), _p(q), _p(r), C.byref(nd)))
+        return q.T, r.T, nd.value
+
+    def gn_solve(self, mode="SketchPrec", method=RANDSVD, rank=10, rank2=-1, growth=5, max_rank=-1,
+                 eps_sketch=1.5, eps_reuse=10.0, seed=0, grad_tol=1e-6, pcg_tol=1e-9, max_gn_iters=50,
+                 pcg_max_iter=10000, max_eig=256):
+        cfg = GNConfigC(MODES[mode] if isinstance(mode, str) else mode, method, rank, rank2, growth, max_rank,
+                        eps_sketch, eps_reuse, seed, grad_tol, pcg_tol, max_gn_iters, pcg_max_iter)
+        analysis = np.empty(self.n)
+        log = np.zeros((64, 16))
+        n_it = C.c_int()
+        summary = np.zeros(5)
+        eig0 = np.full(max_eig, np.nan)
+        check(lib().sdv_gn_solve(self._h, C.byref(cfg), _p(analysis), _p(log), 64, C.byref(n_it), _p(summary),
+                                 _p(eig0), max_eig))
+        return dict(analysis=analysis, log=log[:n_it.value], summary=summary, eig0=eig0[~np.isnan(eig0)])
+
+    def synchronize(self):
+        check(lib().sdv_synchronize(self._h))
+
+
+class Trajectory:
+    """Frozen device linearization (LinearizedTrajectory) + its MisfitOperator."""
+
+    def __init__(self, problem, handle):
+        self.problem = problem
+        self._h = handle
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            lib().sdv_traj_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def total_steps(self):
+        return self.problem.total_steps
+
+    def state_at(self, step):
+        out = np.empty(self.problem.n)
+        check(lib().sdv_traj_state_at(self._h, step, _p(out)))
+        return out
+
+    def tlm_range(self, begin, end, dx):
+        dx = _f64(np.atleast_2d(dx))
+        out = np.empty_like(dx)
+        check(lib().sdv_tlm_range(self._h, begin, end, _p(dx), dx.shape[0], _p(out)))
+        return out
+
+    def adj_range(self, begin, end, lam):
+        lam = _f64(np.atleast_2d(lam))
+        out = np.empty_like(lam)
+        check(lib().sdv_adj_range(self._h, begin, end, _p(lam), lam.shape[0], _p(out)))
+        return out
+
+    # MisfitOperator (apply_columns batched)
+    def misfit_apply(self, V):
+        V = _f64(np.atleast_2d(V))
+        out = np.empty((V.shape[0], self.problem.m))
+        check(lib().sdv_misfit_apply_block(self._h, _p(V), V.shape[0], _p(out)))
+        return out
+
+    def misfit_adjoint(self, W):
+        W = _f64(np.atleast_2d(W))
+        out = np.empty((W.shape[0], self.problem.n))
+        check(lib().sdv_misfit_adjoint_block(self._h, _p(W), W.shape[0], _p(out)))
+        return out
+
+    def gram(self, V):
+        V = _f64(np.atleast_2d(V))
+        out = np.empty_like(V)
+        check(lib().sdv_gram_apply_block(self._h, _p(V), V.shape[0], _p(out)))
+        return out
+
+    def gram_dev(self, v_dev, s, out_dev):
+        check(lib().sdv_gram_apply_block_dev(self._h, C.c_void_p(v_dev), s, C.c_void_p(out_dev)))
+
+    def sketch(self, method, rank, seed, rank2=-1, want_basis=True):
+        eig = np.empty(rank)
+        basis = np.empty((rank, self.problem.n)) if want_basis else None
+        counts = np.zeros(3, np.int64)
+        check(lib().sdv_sketch(self._h, method, rank, rank2, seed, _p(eig), _p(basis), counts.ctypes.data_as(I64)))
+        k = int(counts[2])
+        return eig[:k], (basis[:k] if basis is not None else None), counts
+
+    def pcg_solve(self, rhs, basis=None, eig=None, tol=1e-9, max_iter=10000):
+        l = 0 if basis is None else np.atleast_2d(basis).shape[0]
+        x = np.empty(self.problem.n)
+        info = np.zeros(2, np.int32)
+        check(lib().sdv_pcg_solve(self._h, _p(_f64(rhs)), l, _p(None if basis is None else _f64(basis)),
+                                  _p(None if eig is None else _f64(eig)), tol, max_iter, _p(x),
+                                  info.ctypes.data_as(I32)))
+        return x, int(info[0]), bool(info[1])
+
+
+class DeviceBuffer:
+    """Raw device allocation (for device-resident benchmark inputs)."""
+
+    def __init__(self, nbytes):
+        self.ptr = C.c_void_p()
+        self.nbytes = nbytes
+        check(lib().sdv_dev_alloc(nbytes, C.byref(self.ptr)))
+
+    def upload(self, arr):
+        a = np.ascontiguousarray(arr)
+        check(lib().sdv_memcpy_htod(self.ptr, a.ctypes.data_as(C.c_void_p), a.nbytes))
+
+    def download(self, shape, dtype=np.float64):
+        out = np.empty(shape, dtype)
+        check(lib().sdv_memcpy_dtoh(out.ctypes.data_as(C.c_void_p), self.ptr, out.nbytes))
+        return out
+
+    def free(self):
+        if self.ptr:
+            lib().sdv_dev_free(self.ptr)
+            self.ptr = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class PinnedBuffer:
+    """Page-locked host buffer viewed as a numpy array."""
+
+    def __init__(self, shape, dtype=np.float64):
+        nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        self.ptr = C.c_void_p()
+        check(lib().sdv_host_alloc(nbytes, C.byref(self.ptr)))
+        buf = (C.c_char * nbytes).from_address(self.ptr.value)
+        self.array = np.frombuffer(buf, dtype=dtype).reshape(shape)
+
+    def free(self):
+        if self.ptr:
+            self.array = None
+            lib().sdv_host_free(self.ptr)
+            self.ptr = C.c_void_p()

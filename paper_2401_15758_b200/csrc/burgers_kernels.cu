@@ -1,0 +1,271 @@
+// Batched fp64 1-D viscous Burgers RK4 TLM / ADJ / FWD sweeps, sm_100a.
+//
+// Replaces BurgersTrajectory::tlm_range / adj_range + step_tlm / step_adj +
+// rhs_jacobian(_adjoint) (/root/reference/proj/src/burgers.cpp:152-236) for
+// the periodic RK4 configs. One CTA owns one
+// vector of the block for the whole sweep: the tangent/adjoint field lives in
+// registers + shared memory across all stages (no HBM round trip per stage);
+// the stored base stage inputs u_s, [steps][4][n], are streamed from L2/HBM
+// and are shared by every CTA of the block at the same step.
+// Observation gathers (TLM) and scatters (ADJ) are fused at interval ends.
+#include "burgers_kernels.cuh"
+#include "fft.cuh"
+
+#include <type_traits>
+
+namespace sdv {
+
+namespace {
+__device__ __forceinline__ int wrapm(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
+}  // namespace
+
+// Forward nonlinear sweep (one vector). Stores the 4 RK4 stage inputs of
+// every step in base (if non-null) and the final state in out.
+template <int NPT>
+__global__ void __launch_bounds__(1024) burgers_fwd_kernel(BurgersArgs p, const double* __restrict__ x0,
+                                                           double* __restrict__ base, double* __restrict__ out,
+                                                           int steps) {
+  extern __shared__ double sh[];
+  double* X = sh;
+  const int n = p.n, tid = threadIdx.x, nt = blockDim.x;
+  double U[NPT], A[NPT];
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) U[q] = x0[tid + q * nt];
+  for (int k = 0; k < steps; ++k) {
+    for (int s = 0; s < 4; ++s) {
+      double xs[NPT];
+      if (s == 0) {
+#pragma unroll
+        for (int q = 0; q < NPT; ++q) X[tid + q * nt] = U[q];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) {
+        const int i = tid + q * nt, im = wrapm(i - 1, n), ip = wrapm(i + 1, n);
+        const double xi = X[i], xm = X[im], xp = X[ip];
+        if (base) base[(static_cast<long long>(k) * 4 + s) * n + i] = xi;
+        const double kk = -xi * (xp - xm) * p.c1 + p.nu * (xm - 2.0 * xi + xp) * p.c2;
+        switch (s) {
+          case 0: A[q] = U[q] + p.dt / 6.0 * kk; xs[q] = U[q] + 0.5 * p.dt * kk; break;
+          case 1: A[q] += p.dt / 3.0 * kk; xs[q] = U[q] + 0.5 * p.dt * kk; break;
+          case 2: A[q] += p.dt / 3.0 * kk; xs[q] = U[q] + p.dt * kk; break;
+          default: U[q] = A[q] + p.dt / 6.0 * kk; break;
+        }
+      }
+      __syncthreads();
+      if (s < 3) {
+#pragma unroll
+        for (int q = 0; q < NPT; ++q) X[tid + q * nt] = xs[q];
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) out[tid + q * nt] = U[q];
+}
+
+// Block TLM over steps [k0, k1). state: [nvec][n] in/out.
+template <int NPT>
+__global__ void __launch_bounds__(1024) burgers_tlm_kernel(BurgersArgs p, double* __restrict__ state) {
+  extern __shared__ double sh[];
+  double* X = sh;
+  const int n = p.n, tid = threadIdx.x, nt = blockDim.x;
+  const long long v = blockIdx.x;
+  double D[NPT], A[NPT];
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) D[q] = state[v * n + tid + q * nt];
+  for (int k = p.k0; k < p.k1; ++k) {
+    const double* ub = p.base + static_cast<long long>(k) * 4 * n;
+    for (int s = 0; s < 4; ++s) {
+      double xs[NPT];
+      if (s == 0) {
+#pragma unroll
+        for (int q = 0; q < NPT; ++q) X[tid + q * nt] = D[q];
+      }
+      __syncthreads();
+      const double* u = ub + s * n;
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) {
+        const int i = tid + q * nt, im = wrapm(i - 1, n), ip = wrapm(i + 1, n);
+        const double xi = X[i], xm = X[im], xp = X[ip];
+        const double ui = __ldg(u + i), um = __ldg(u + im), up = __ldg(u + ip);
+        const double kk = -xi * (up - um) * p.c1 - ui * (xp - xm) * p.c1 + p.nu * (xm - 2.0 * xi + xp) * p.c2;
+        switch (s) {
+          case 0: A[q] = D[q] + p.dt / 6.0 * kk; xs[q] = D[q] + 0.5 * p.dt * kk; break;
+          case 1: A[q] += p.dt / 3.0 * kk; xs[q] = D[q] + 0.5 * p.dt * kk; break;
+          case 2: A[q] += p.dt / 3.0 * kk; xs[q] = D[q] + p.dt * kk; break;
+          default: D[q] = A[q] + p.dt / 6.0 * kk; break;
+        }
+      }
+      __syncthreads();
+      if (s < 3) {
+#pragma unroll
+        for (int q = 0; q < NPT; ++q) X[tid + q * nt] = xs[q];
+      }
+    }
+    if (p.y && (k + 1) % p.spi == 0) {
+      const int iv = (k + 1) / p.spi - 1;
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) X[tid + q * nt] = D[q];
+      __syncthreads();
+      for (int o = tid; o < p.n_obs; o += nt)
+        p.y[v * p.m + static_cast<long long>(iv) * p.n_obs + o] = X[p.idx[o]] * p.w[static_cast<long long>(iv) * p.n_obs + o];
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) state[v * n + tid + q * nt] = D[q];
+}
+
+// Block ADJ over steps [k0, k1) backwards:
+//   a4 = dt/6 L, m4 = J4^T a4; a3 = dt/3 L + dt m4, ...; L <- L + sum m.
+// Observation scatter L[idx] += y*w before each interval's last step.
+template <int NPT>
+__global__ void __launch_bounds__(1024) burgers_adj_kernel(BurgersArgs p, double* __restrict__ state) {
+  extern __shared__ double sh[];
+  double* L = sh;
+  double* Ash = sh + p.n;
+  const int n = p.n, tid = threadIdx.x, nt = blockDim.x;
+  const long long v = blockIdx.x;
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) L[tid + q * nt] = state[v * n + tid + q * nt];
+  __syncthreads();
+  for (int k = p.k1 - 1; k >= p.k0; --k) {
+    if (p.y && (k + 1) % p.spi == 0) {
+      const int iv = (k + 1) / p.spi - 1;
+      for (int o = tid; o < p.n_obs; o += nt)
+        L[p.idx[o]] += p.y[v * p.m + static_cast<long long>(iv) * p.n_obs + o] * p.w[static_cast<long long>(iv) * p.n_obs + o];
+      __syncthreads();
+    }
+    const double* ub = p.base + static_cast<long long>(k) * 4 * n;
+    double acc[NPT], mu[NPT];
+    for (int s = 3; s >= 0; --s) {
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) {
+        const double l = L[tid + q * nt];
+        double a;
+        switch (s) {
+          case 3: a = p.dt / 6.0 * l; break;
+          case 2: a = p.dt / 3.0 * l + p.dt * mu[q]; break;
+          case 1: a = p.dt / 3.0 * l + 0.5 * p.dt * mu[q]; break;
+          default: a = p.dt / 6.0 * l + 0.5 * p.dt * mu[q]; break;
+        }
+        Ash[tid + q * nt] = a;
+      }
+      __syncthreads();
+      const double* u = ub + s * n;
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) {
+        const int i = tid + q * nt, im = wrapm(i - 1, n), ip = wrapm(i + 1, n);
+        const double ai = Ash[i], am = Ash[im], ap = Ash[ip];
+        const double ui = __ldg(u + i), um = __ldg(u + im), up = __ldg(u + ip);
+        const double m = -ai * (up - um) * p.c1 + (up * ap - um * am) * p.c1 + p.nu * (am - 2.0 * ai + ap) * p.c2;
+        mu[q] = m;
+        acc[q] = (s == 3) ? m : acc[q] + m;
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) L[tid + q * nt] += acc[q];
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) state[v * n + tid + q * nt] = L[tid + q * nt];
+}
+
+// 1-D periodic circulant apply out = Re IFFT(sym .* FFT(in)), one CTA per vector.
+template <int N>
+__global__ void __launch_bounds__(1024) spectral1d_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                                          const double* __restrict__ sym, const double2* __restrict__ tw) {
+  constexpr int kTeam = N / 4 < 1024 ? N / 4 : 1024;
+  extern __shared__ double2 sm2[];
+  double2* a = sm2;
+  double2* b = sm2 + N;
+  const long long v = blockIdx.x;
+  const int t = threadIdx.x;
+  for (int x = t; x < N; x += kTeam) a[x] = make_double2(in[v * N + x], 0.0);
+  __syncthreads();
+  double2* z = fft_team<N, false>(a, b, tw, t, kTeam, true);
+  for (int k = t; k < N; k += kTeam) {
+    const double w = sym[k];
+    z[k] = make_double2(w * z[k].x, w * z[k].y);
+  }
+  __syncthreads();
+  double2* o = (z == a) ? b : a;
+  double2* r = fft_team<N, true>(z, o, tw, t, kTeam, true);
+  for (int x = t; x < N; x += kTeam) out[v * N + x] = r[x].x;
+}
+
+namespace {
+template <class F>
+void dispatch_npt(int npt, F&& f) {
+  switch (npt) {
+    case 1: f(std::integral_constant<int, 1>{}); break;
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    case 8: f(std::integral_constant<int, 8>{}); break;
+    default: throw std::invalid_argument("Burgers: n must be a power of two in [32, 4096]");
+  }
+}
+void geometry(int n, int& threads, int& npt) {
+  if (n < 32 || (n & (n - 1)) || n > 4096) throw std::invalid_argument("Burgers: n must be a power of two in [32, 4096]");
+  threads = n < 1024 ? n : 1024;
+  npt = n / threads;
+}
+}  // namespace
+
+void burgers_fwd(const BurgersArgs& p, const double* x0, double* base, double* out, int steps, cudaStream_t st) {
+  int th, npt;
+  geometry(p.n, th, npt);
+  dispatch_npt(npt, [&](auto c) {
+    burgers_fwd_kernel<decltype(c)::value><<<1, th, sizeof(double) * p.n, st>>>(p, x0, base, out, steps);
+  });
+  SDV_LAUNCH_CHECK();
+}
+void burgers_tlm(const BurgersArgs& p, double* state, int nvec, cudaStream_t st) {
+  int th, npt;
+  geometry(p.n, th, npt);
+  dispatch_npt(npt, [&](auto c) {
+    burgers_tlm_kernel<decltype(c)::value><<<nvec, th, sizeof(double) * p.n, st>>>(p, state);
+  });
+  SDV_LAUNCH_CHECK();
+}
+void burgers_adj(const BurgersArgs& p, double* state, int nvec, cudaStream_t st) {
+  int th, npt;
+  geometry(p.n, th, npt);
+  dispatch_npt(npt, [&](auto c) {
+    burgers_adj_kernel<decltype(c)::value><<<nvec, th, sizeof(double) * 2 * p.n, st>>>(p, state);
+  });
+  SDV_LAUNCH_CHECK();
+}
+
+namespace {
+template <int N>
+void spectral1d_launch(const double* in, double* out, const double* sym, int nvec, cudaStream_t st) {
+  constexpr int kTeam = N / 4 < 1024 ? N / 4 : 1024;
+  const size_t smem = sizeof(double2) * 2 * N;
+  static bool init = false;
+  if (!init) {
+    SDV_CUDA(cudaFuncSetAttribute(spectral1d_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    init = true;
+  }
+  spectral1d_kernel<N><<<nvec, kTeam, smem, st>>>(in, out, sym, twiddle_table(N));
+  SDV_LAUNCH_CHECK();
+}
+}  // namespace
+
+void spectral1d(int n, const double* in, double* out, const double* sym, int nvec, cudaStream_t st) {
+  switch (n) {
+    case 32: spectral1d_launch<32>(in, out, sym, nvec, st); break;
+    case 64: spectral1d_launch<64>(in, out, sym, nvec, st); break;
+    case 128: spectral1d_launch<128>(in, out, sym, nvec, st); break;
+    case 256: spectral1d_launch<256>(in, out, sym, nvec, st); break;
+    case 512: spectral1d_launch<512>(in, out, sym, nvec, st); break;
+    case 1024: spectral1d_launch<1024>(in, out, sym, nvec, st); break;
+    case 2048: spectral1d_launch<2048>(in, out, sym, nvec, st); break;
+    case 4096: spectral1d_launch<4096>(in, out, sym, nvec, st); break;
+    default: throw std::invalid_argument("spectral1d: n must be a power of two in [32, 4096]");
+  }
+}
+
+}  // namespace sdv

@@ -1,0 +1,464 @@
+// Device-resident problem, base trajectory and batched Hessian-product sweeps.
+//
+// Reference correspondence (/root/reference/proj):
+//   Problem::linearize      <- DynamicalModel::linearize (include/sketchdav/model.hpp:36-40),
+//                              BurgersTrajectory/BVETrajectory ctors (src/burgers.cpp:114-138, src/bve.cpp:103-127)
+//   Problem::tlm / adj      <- LinearizedTrajectory::tlm_range / adj_range (src/burgers.cpp:152-191,
+//                              src/bve.cpp:138-161), batched over s vectors
+//   Problem::misfit_apply   <- MisfitOperator::apply (src/fourdvar.cpp:145-160)
+//   Problem::misfit_adjoint <- MisfitOperator::adjoint_apply (src/fourdvar.cpp:162-176)
+//   Problem::gram_apply     <- GramMap::apply (include/sketchdav/linalg.hpp:72-74)
+//   Problem::evaluate       <- evaluate (src/fourdvar.cpp:92-132), control-variable background term
+//   Problem::prior_sqrt     <- PriorCovariance::apply_sqrt (src/prior.cpp:64-69), Fourier-diagonal B
+#include <cmath>
+#include <map>
+#include <mutex>
+
+#include "engine.hpp"
+#include "fft.cuh"
+
+namespace sdv {
+
+// ------------------------------------------------------------ twiddles ------
+const double2* twiddle_table(int n) {
+  static std::mutex mu;
+  static std::map<int, double2*> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(n);
+  if (it != cache.end()) return it->second;
+  std::vector<double2> h(static_cast<size_t>(n));
+  for (int m = 0; m < n; ++m) {
+    const double ang = -2.0 * M_PI * static_cast<double>(m) / static_cast<double>(n);
+    h[m] = make_double2(std::cos(ang), std::sin(ang));
+  }
+  double2* d = nullptr;
+  SDV_CUDA(cudaMalloc(&d, sizeof(double2) * n));
+  SDV_CUDA(cudaMemcpy(d, h.data(), sizeof(double2) * n, cudaMemcpyHostToDevice));
+  cache[n] = d;
+  return d;
+}
+
+namespace {
+
+__global__ void innovation_kernel(const double* __restrict__ f, const long long* __restrict__ idx, int n_obs,
+                                  const double* __restrict__ values, const double* __restrict__ rinv,
+                                  double* __restrict__ innov, double* __restrict__ winnov) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_obs) return;
+  const double d = f[idx[k]] - values[k];
+  innov[k] = d;
+  winnov[k] = d * rinv[k];
+}
+
+bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+// Fourier symbols, computed exactly as the oracle's FourierPrior /
+// PeriodicBVE (identical expression order, so the tables agree bitwise).
+std::vector<double> fourier_b_full(int n, int dims, double sigma, double len) {
+  const size_t nn = dims == 1 ? static_cast<size_t>(n) : static_cast<size_t>(n) * n;
+  std::vector<double> c(nn), sym(nn);
+  double sum = 0.0;
+  auto kk = [n](int k) { return k <= n / 2 ? k : k - n; };
+  for (size_t idx = 0; idx < nn; ++idx) {
+    double e;
+    if (dims == 1) {
+      const double k = kk(static_cast<int>(idx));
+      e = std::exp(-0.5 * (2.0 * M_PI * k * len) * (2.0 * M_PI * k * len));
+    } else {
+      const double kx = kk(static_cast<int>(idx % n)), ky = kk(static_cast<int>(idx / n));
+      e = std::exp(-0.5 * (kx * kx + ky * ky) * len * len);
+    }
+    c[idx] = e;
+    sum += e;
+  }
+  for (size_t idx = 0; idx < nn; ++idx) {
+    const double chat = c[idx] * static_cast<double>(nn) / sum;
+    sym[idx] = sigma * std::sqrt(chat) / static_cast<double>(nn);
+  }
+  return sym;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- problem ------
+Problem::Problem(const ProblemDesc& d, long long n_obs, const long long* idx, const double* values,
+                 const double* variances, const double* background)
+    : d_(d), n_obs_(n_obs) {
+  if (d.model != kModelBurgers && d.model != kModelBVE) throw std::invalid_argument("problem: unknown model kind");
+  if (!is_pow2(d.n) || d.n < 32 || (d.model == kModelBurgers && d.n > 4096) || (d.model == kModelBVE && d.n > 512))
+    throw std::invalid_argument("problem: n must be a power of two (Burgers 32..4096, BVE 32..512)");
+  if (!(d.nu >= 0.0) || !(d.dt > 0.0)) throw std::invalid_argument("problem: need nu >= 0 and dt > 0");
+  if (d.n_t < 1 || d.spi < 1) throw std::invalid_argument("AssimilationProblem: need n_t >= 1 and steps_per_interval >= 1");
+  if (!(d.prior_sigma > 0.0) || !(d.prior_length > 0.0)) throw std::invalid_argument("problem: prior sigma/length must be positive");
+  dim_ = d.model == kModelBurgers ? d.n : static_cast<long long>(d.n) * d.n;
+  if (n_obs < 0 || n_obs > dim_) throw std::invalid_argument("AssimilationProblem: n_obs > n");
+  long long prev = -1;
+  for (long long k = 0; k < n_obs; ++k) {
+    if (idx[k] <= prev || idx[k] >= dim_)
+      throw std::invalid_argument(
+          "AssimilationProblem: observation indices must be strictly increasing and in range");
+    prev = idx[k];
+  }
+  const long long m = n_obs * d.n_t;
+  std::vector<double> rs(static_cast<size_t>(m)), ri(static_cast<size_t>(m));
+  for (long long i = 0; i < m; ++i) {
+    if (!(variances[i] > 0.0)) throw std::invalid_argument("AssimilationProblem: observation variances must be positive");
+    rs[i] = 1.0 / std::sqrt(variances[i]);
+    ri[i] = 1.0 / variances[i];
+  }
+  SDV_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  idx_.upload(idx, static_cast<size_t>(std::max<long long>(n_obs, 1)), st_);
+  values_.upload(values, static_cast<size_t>(std::max<long long>(m, 1)), st_);
+  rinv_sqrt_.upload(rs.data(), static_cast<size_t>(std::max<long long>(m, 1)), st_);
+  rinv_.upload(ri.data(), static_cast<size_t>(std::max<long long>(m, 1)), st_);
+  background_.upload(background, static_cast<size_t>(dim_), st_);
+  const int n = d.n;
+  if (d.model == kModelBurgers) {
+    const std::vector<double> sb = fourier_b_full(n, 1, d.prior_sigma, d.prior_length);
+    sym_b_.upload(sb.data(), sb.size(), st_);
+  } else {
+    const std::vector<double> full = fourier_b_full(n, 2, d.prior_sigma, d.prior_length);
+    std::vector<double> sb(static_cast<size_t>(n / 2 + 1) * n), sp(sb.size());
+    const double h = 2.0 * M_PI / n;
+    for (int kx = 0; kx <= n / 2; ++kx)
+      for (int ky = 0; ky < n; ++ky) {
+        sb[static_cast<size_t>(kx) * n + ky] = full[kx + static_cast<size_t>(n) * ky];
+        const double sx = std::sin(M_PI * kx / n), sy = std::sin(M_PI * ky / n);
+        const double mu = 4.0 / (h * h) * (sx * sx + sy * sy);
+        sp[static_cast<size_t>(kx) * n + ky] = (kx == 0 && ky == 0) ? 0.0 : 1.0 / (mu * static_cast<double>(n) * n);
+      }
+    sym_b_.upload(sb.data(), sb.size(), st_);
+    sym_p_.upload(sp.data(), sp.size(), st_);
+  }
+  SDV_CUDA(cudaStreamSynchronize(st_));
+}
+
+int Problem::group() const {
+  if (d_.model != kModelBVE) return 1 << 30;
+  if (d_.block_group > 0) return d_.block_group;
+  // Keep a group's sweep working set (D, A, X0, X1, S0, S1 ~ 6 fields per
+  // vector) within ~80 MB of the 126 MB L2.
+  const double per = 6.0 * 8.0 * static_cast<double>(dim_);
+  return std::max(1, static_cast<int>(80e6 / per));
+}
+
+void Problem::ensure_work(int nvec) const {
+  if (d_.model != kModelBVE) return;
+  const int g = std::min(nvec, group());
+  if (g <= work_nvec_) return;
+  const size_t f = static_cast<size_t>(g) * dim_;
+  wa_.alloc(f);
+  wx0_.alloc(f);
+  wx1_.alloc(f);
+  ws0_.alloc(static_cast<size_t>(g) * d_.n * (d_.n / 2));
+  ws1_.alloc(static_cast<size_t>(g) * d_.n * (d_.n / 2));
+  work_nvec_ = g;
+}
+
+const double* Trajectory::state_at(int step) const {
+  if (step < 0 || step > steps) throw std::invalid_argument("trajectory: step out of range");
+  if (step == steps) return final.get();
+  return w.get() + static_cast<long long>(step) * 4 * prob->dim();
+}
+
+namespace {
+BurgersArgs burgers_args(const ProblemDesc& d) {
+  BurgersArgs a;
+  a.n = d.n;
+  a.dt = d.dt;
+  a.nu = d.nu;
+  a.c1 = 0.5 * d.n;
+  a.c2 = static_cast<double>(d.n) * d.n;
+  a.spi = d.spi;
+  return a;
+}
+StageArgs bve_args(const ProblemDesc& d) {
+  StageArgs a;
+  const double h = 2.0 * M_PI / d.n;
+  a.dt = d.dt;
+  a.nu = d.nu;
+  a.inv12h2 = 1.0 / (12.0 * h * h);
+  a.invh2 = 1.0 / (h * h);
+  a.tw = twiddle_table(d.n);
+  return a;
+}
+}  // namespace
+
+void Problem::forward(const double* d_x0, int steps, double* d_out) const {
+  if (d_.model == kModelBurgers) {
+    burgers_fwd(burgers_args(d_), d_x0, nullptr, d_out, steps, st_);
+    count_launch();
+    return;
+  }
+  ensure_work(1);
+  const int n = d_.n;
+  double* u = d_out;
+  if (u != d_x0) SDV_CUDA(cudaMemcpyAsync(u, d_x0, sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
+  double2* s_cur = ws0_.get();
+  double2* s_nxt = ws1_.get();
+  bve_row_fwd(n, u, s_cur, 1, st_);
+  count_launch();
+  double* xb[2] = {wx0_.get(), wx1_.get()};
+  for (int k = 0; k < steps; ++k)
+    for (int s = 0; s < 4; ++s) {
+      bve_col(n, s_cur, sym_p_.get(), 1, st_);
+      StageArgs a = bve_args(d_);
+      a.stage = s;
+      a.s_in = s_cur;
+      a.s_out = s_nxt;
+      a.x_in = s == 0 ? u : xb[(s - 1) & 1];
+      a.x_out = s < 3 ? xb[s & 1] : nullptr;
+      a.d = u;
+      a.acc = wa_.get();
+      bve_stage(n, kModeNl, a, 1, st_);
+      count_launch(2);
+      std::swap(s_cur, s_nxt);
+    }
+}
+
+std::unique_ptr<Trajectory> Problem::linearize(const double* d_x0) const {
+  auto tr = std::make_unique<Trajectory>();
+  tr->prob = this;
+  tr->steps = total_steps();
+  const long long st_elems = static_cast<long long>(tr->steps) * 4 * dim_;
+  tr->w.alloc(static_cast<size_t>(st_elems));
+  tr->final.alloc(static_cast<size_t>(dim_));
+  if (d_.model == kModelBurgers) {
+    burgers_fwd(burgers_args(d_), d_x0, tr->w.get(), tr->final.get(), tr->steps, st_);
+    count_launch();
+  } else {
+    tr->p.alloc(static_cast<size_t>(st_elems));
+    ensure_work(1);
+    const int n = d_.n;
+    double* u = tr->final.get();
+    SDV_CUDA(cudaMemcpyAsync(u, d_x0, sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
+    double2* s_cur = ws0_.get();
+    double2* s_nxt = ws1_.get();
+    bve_row_fwd(n, u, s_cur, 1, st_);
+    count_launch();
+    double* xb[2] = {wx0_.get(), wx1_.get()};
+    for (int k = 0; k < tr->steps; ++k)
+      for (int s = 0; s < 4; ++s) {
+        bve_col(n, s_cur, sym_p_.get(), 1, st_);
+        StageArgs a = bve_args(d_);
+        a.stage = s;
+        a.s_in = s_cur;
+        a.s_out = s_nxt;
+        a.x_in = s == 0 ? u : xb[(s - 1) & 1];
+        a.x_out = s < 3 ? xb[s & 1] : nullptr;
+        a.d = u;
+        a.acc = wa_.get();
+        a.store_w = tr->w.get() + (static_cast<long long>(k) * 4 + s) * dim_;
+        a.store_p = tr->p.get() + (static_cast<long long>(k) * 4 + s) * dim_;
+        bve_stage(n, kModeNl, a, 1, st_);
+        count_launch(2);
+        std::swap(s_cur, s_nxt);
+      }
+  }
+  // Non-finite check on the final state (reference throws on NaN/Inf,
+  // proj/src/burgers.cpp:128-131, proj/src/bve.cpp:120-124).
+  DevBuf<double> r(1);
+  dev_dot(tr->final.get(), tr->final.get(), dim_, r.get(), st_);
+  double nn = 0.0;
+  SDV_CUDA(cudaMemcpyAsync(&nn, r.get(), sizeof(double), cudaMemcpyDeviceToHost, st_));
+  SDV_CUDA(cudaStreamSynchronize(st_));
+  if (!std::isfinite(nn))
+    throw std::runtime_error("linearize: non-finite state (time step too large for stability)");
+  return tr;
+}
+
+void Problem::prior_sqrt(const double* in, double* out, int nvec) const {
+  if (d_.model == kModelBurgers) {
+    spectral1d(d_.n, in, out, sym_b_.get(), nvec, st_);
+    count_launch();
+    return;
+  }
+  ensure_work(nvec);
+  const int g = std::min(nvec, group());
+  for (int v0 = 0; v0 < nvec; v0 += g) {
+    const int gn = std::min(g, nvec - v0);
+    bve_row_fwd(d_.n, in + v0 * dim_, ws0_.get(), gn, st_);
+    bve_col(d_.n, ws0_.get(), sym_b_.get(), gn, st_);
+    bve_row_inv(d_.n, ws0_.get(), out + v0 * dim_, gn, st_);
+    count_launch(3);
+  }
+}
+
+void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1, double* y, const double* w) const {
+  if (k0 < 0 || k1 > tr.steps || k0 > k1) throw std::invalid_argument("trajectory: step range out of bounds");
+  if (y && k0 != 0) throw std::invalid_argument("tlm: observation gathers need k0 == 0");
+  if (nvec <= 0 || k0 == k1) return;
+  if (d_.model == kModelBurgers) {
+    BurgersArgs a = burgers_args(d_);
+    a.base = tr.w.get();
+    a.k0 = k0;
+    a.k1 = k1;
+    a.idx = idx_.get();
+    a.n_obs = static_cast<int>(n_obs_);
+    a.w = w;
+    a.y = y;
+    a.m = m();
+    burgers_tlm(a, state, nvec, st_);
+    count_launch();
+    return;
+  }
+  ensure_work(nvec);
+  const int n = d_.n, g = std::min(nvec, group());
+  double* xb[2] = {wx0_.get(), wx1_.get()};
+  for (int v0 = 0; v0 < nvec; v0 += g) {
+    const int gn = std::min(g, nvec - v0);
+    double* dst = state + v0 * dim_;
+    double2* s_cur = ws0_.get();
+    double2* s_nxt = ws1_.get();
+    bve_row_fwd(n, dst, s_cur, gn, st_);
+    count_launch();
+    for (int k = k0; k < k1; ++k) {
+      for (int s = 0; s < 4; ++s) {
+        bve_col(n, s_cur, sym_p_.get(), gn, st_);
+        StageArgs a = bve_args(d_);
+        a.stage = s;
+        a.s_in = s_cur;
+        a.s_out = s_nxt;
+        a.x_in = s == 0 ? dst : xb[(s - 1) & 1];
+        a.x_out = s < 3 ? xb[s & 1] : nullptr;
+        a.d = dst;
+        a.acc = wa_.get();
+        a.base_w = tr.w.get() + (static_cast<long long>(k) * 4 + s) * dim_;
+        a.base_p = tr.p.get() + (static_cast<long long>(k) * 4 + s) * dim_;
+        bve_stage(n, kModeTlm, a, gn, st_);
+        count_launch(2);
+        std::swap(s_cur, s_nxt);
+      }
+      if (y && (k + 1) % d_.spi == 0) {
+        const int iv = (k + 1) / d_.spi - 1;
+        gather_obs(dst, dim_, idx_.get(), static_cast<int>(n_obs_), w + static_cast<long long>(iv) * n_obs_,
+                   y + v0 * m() + static_cast<long long>(iv) * n_obs_, m(), gn, st_);
+        count_launch();
+      }
+    }
+  }
+}
+
+void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1, const double* y,
+                  const double* w) const {
+  if (k0 < 0 || k1 > tr.steps || k0 > k1) throw std::invalid_argument("trajectory: step range out of bounds");
+  if (nvec <= 0 || k0 == k1) return;
+  if (d_.model == kModelBurgers) {
+    BurgersArgs a = burgers_args(d_);
+    a.base = tr.w.get();
+    a.k0 = k0;
+    a.k1 = k1;
+    a.idx = idx_.get();
+    a.n_obs = static_cast<int>(n_obs_);
+    a.w = w;
+    a.y = const_cast<double*>(y);
+    a.m = m();
+    burgers_adj(a, state, nvec, st_);
+    count_launch();
+    return;
+  }
+  ensure_work(nvec);
+  const int n = d_.n, g = std::min(nvec, group());
+  double* qb[2] = {wx0_.get(), wx1_.get()};
+  for (int v0 = 0; v0 < nvec; v0 += g) {
+    const int gn = std::min(g, nvec - v0);
+    double* lam = state + v0 * dim_;
+    double* acc = wa_.get();
+    double2* s_cur = ws0_.get();
+    double2* s_nxt = ws1_.get();
+    int qi = 0;
+    bool first = true;
+    for (int k = k1 - 1; k >= k0; --k) {
+      if (y && (k + 1) % d_.spi == 0) {
+        const int iv = (k + 1) / d_.spi - 1;
+        scatter_obs(first ? lam : acc, dim_, idx_.get(), static_cast<int>(n_obs_),
+                    w + static_cast<long long>(iv) * n_obs_, y + v0 * m() + static_cast<long long>(iv) * n_obs_, m(),
+                    gn, st_);
+        count_launch();
+      }
+      for (int s = 3; s >= 0; --s) {
+        const bool has_prev = !first;
+        if (has_prev) {
+          bve_col(n, s_cur, sym_p_.get(), gn, st_);
+          count_launch();
+        }
+        StageArgs a = bve_args(d_);
+        a.stage = s;
+        a.flags = has_prev ? kFlagHasPrev : 0;
+        a.s_in = s_cur;
+        a.s_out = s_nxt;
+        a.d = lam;
+        a.acc = acc;
+        a.q_in = qb[qi];
+        a.q_out = qb[qi ^ 1];
+        a.base_w = tr.w.get() + (static_cast<long long>(k) * 4 + s) * dim_;
+        a.base_p = tr.p.get() + (static_cast<long long>(k) * 4 + s) * dim_;
+        bve_stage(n, kModeAdj, a, gn, st_);
+        count_launch();
+        std::swap(s_cur, s_nxt);
+        qi ^= 1;
+        first = false;
+      }
+    }
+    bve_col(n, s_cur, sym_p_.get(), gn, st_);
+    StageArgs a = bve_args(d_);
+    a.flags = kFlagHasPrev | kFlagFinish;
+    a.s_in = s_cur;
+    a.d = lam;
+    a.acc = acc;
+    a.q_in = qb[qi];
+    bve_stage(n, kModeAdj, a, gn, st_);
+    count_launch(2);
+  }
+}
+
+void Problem::misfit_apply(const Trajectory& tr, const double* v, int s, double* y) const {
+  wstate_.ensure(static_cast<size_t>(s) * dim_);
+  prior_sqrt(v, wstate_.get(), s);
+  tlm(tr, wstate_.get(), s, 0, total_steps(), y, rinv_sqrt_.get());
+}
+
+void Problem::misfit_adjoint(const Trajectory& tr, const double* w, int s, double* z) const {
+  wstate_.ensure(static_cast<size_t>(s) * dim_);
+  dev_fill(static_cast<long long>(s) * dim_, 0.0, wstate_.get(), st_);
+  adj(tr, wstate_.get(), s, 0, total_steps(), w, rinv_sqrt_.get());
+  prior_sqrt(wstate_.get(), z, s);
+}
+
+void Problem::gram_apply(const Trajectory& tr, const double* v, int s, double* hv) const {
+  wy_.ensure(static_cast<size_t>(s) * m());
+  misfit_apply(tr, v, s, wy_.get());
+  misfit_adjoint(tr, wy_.get(), s, hv);
+}
+
+double Problem::evaluate(const Trajectory& tr, const double* d_z, double* d_ctrl_grad, double* d_lambda0) const {
+  const long long mm = m();
+  DevBuf<double> innov(static_cast<size_t>(std::max<long long>(mm, 1))), winnov(innov.size()), sc(2),
+      lam(static_cast<size_t>(dim_));
+  for (int i = 1; i <= d_.n_t; ++i) {
+    const long long o = static_cast<long long>(i - 1) * n_obs_;
+    if (n_obs_ > 0) {
+      innovation_kernel<<<ceil_div(n_obs_, 256), 256, 0, st_>>>(tr.state_at(i * d_.spi), idx_.get(),
+                                                                static_cast<int>(n_obs_), values_.get() + o,
+                                                                rinv_.get() + o, innov.get() + o, winnov.get() + o);
+      count_launch();
+      SDV_LAUNCH_CHECK();
+    }
+  }
+  dev_dot(innov.get(), winnov.get(), mm, sc.get(), st_);
+  if (d_z) dev_dot(d_z, d_z, dim_, sc.get() + 1, st_);
+  else dev_fill(1, 0.0, sc.get() + 1, st_);
+  dev_fill(dim_, 0.0, lam.get(), st_);
+  adj(tr, lam.get(), 1, 0, total_steps(), innov.get(), rinv_.get());
+  if (d_lambda0) SDV_CUDA(cudaMemcpyAsync(d_lambda0, lam.get(), sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
+  if (d_ctrl_grad) {
+    prior_sqrt(lam.get(), d_ctrl_grad, 1);
+    if (d_z) dev_axpby(dim_, 1.0, d_z, 1.0, d_ctrl_grad, st_);
+  }
+  double h[2];
+  SDV_CUDA(cudaMemcpyAsync(h, sc.get(), sizeof(h), cudaMemcpyDeviceToHost, st_));
+  SDV_CUDA(cudaStreamSynchronize(st_));
+  return 0.5 * h[1] + 0.5 * h[0];
+}
+
+}  // namespace sdv

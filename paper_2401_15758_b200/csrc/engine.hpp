@@ -1,0 +1,93 @@
+// Host-side engine: the device-resident problem, base trajectory and the
+// batched Hessian-product sweeps. Mirrors the reference interfaces
+//   AssimilationProblem / DynamicalModel::linearize / LinearizedTrajectory
+//   MisfitOperator::apply / adjoint_apply / GramMap
+// (/root/reference/proj/include/sketchdav/{fourdvar,model,linalg}.hpp) with
+// block (s-vector) device entry points.
+#pragma once
+
+#include <memory>
+
+#include "bve_kernels.cuh"
+#include "burgers_kernels.cuh"
+#include "linalg_kernels.cuh"
+
+namespace sdv {
+
+enum ModelKind { kModelBurgers = 1, kModelBVE = 2 };
+
+struct ProblemDesc {
+  int model = kModelBurgers;
+  int n = 0;  // grid points per dimension
+  double nu = 0, dt = 0;
+  int n_t = 0, spi = 0;
+  double prior_sigma = 0, prior_length = 0;
+  int block_group = 0;  // vectors per BVE sweep group (0 = auto)
+};
+
+class Problem;
+
+// Device-resident base trajectory (FWD sweep output).
+struct Trajectory {
+  const Problem* prob = nullptr;
+  int steps = 0;
+  DevBuf<double> w;      // [steps][4][dim] stage inputs
+  DevBuf<double> p;      // BVE: [steps][4][dim] stage streamfunctions
+  DevBuf<double> final;  // [dim]
+  const double* state_at(int step) const;  // step in [0, steps]
+};
+
+class Problem {
+ public:
+  Problem(const ProblemDesc& d, long long n_obs, const long long* idx, const double* values, const double* variances,
+          const double* background);
+  const ProblemDesc& desc() const { return d_; }
+  long long dim() const { return dim_; }
+  long long n_obs() const { return n_obs_; }
+  long long m() const { return n_obs_ * d_.n_t; }
+  int total_steps() const { return d_.n_t * d_.spi; }
+  cudaStream_t stream() const { return st_; }
+
+  // FWD nonlinear sweep from device x0, storing every RK4 stage input.
+  std::unique_ptr<Trajectory> linearize(const double* d_x0) const;
+  // Nonlinear forward of `steps` steps (device in/out), no storage.
+  void forward(const double* d_x0, int steps, double* d_out) const;
+
+  // out = B^{1/2} in, nvec vectors (device).
+  void prior_sqrt(const double* in, double* out, int nvec) const;
+  // TLM over steps [k0,k1) on state (nvec x dim, in/out); gathers obs*w to y
+  // ([nvec][m]) at interval ends when y != null (requires k0 == 0).
+  void tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1, double* y, const double* w) const;
+  // ADJ over [k0,k1) backwards on state (in/out); scatters y*w at interval ends.
+  void adj(const Trajectory& tr, double* state, int nvec, int k0, int k1, const double* y, const double* w) const;
+
+  // Prior-preconditioned misfit operator A = [R^{-1/2} O M Gamma^{1/2}] blocks.
+  void misfit_apply(const Trajectory& tr, const double* v, int s, double* y) const;
+  void misfit_adjoint(const Trajectory& tr, const double* w, int s, double* z) const;
+  void gram_apply(const Trajectory& tr, const double* v, int s, double* hv) const;
+
+  // cost (host), ctrl_grad = z + Gamma^{1/2} lambda0, lambda0 (device, may be null).
+  double evaluate(const Trajectory& tr, const double* d_z, double* d_ctrl_grad, double* d_lambda0) const;
+
+  const double* d_rinv_sqrt() const { return rinv_sqrt_.get(); }
+  const double* d_rinv() const { return rinv_.get(); }
+  const double* d_background() const { return background_.get(); }
+  const long long* d_idx() const { return idx_.get(); }
+
+ private:
+  void ensure_work(int nvec) const;
+  int group() const;
+  ProblemDesc d_;
+  long long dim_ = 0, n_obs_ = 0;
+  cudaStream_t st_ = nullptr;
+  DevBuf<long long> idx_;
+  DevBuf<double> values_, rinv_sqrt_, rinv_, background_;
+  DevBuf<double> sym_b_, sym_p_;
+  double dt_ = 0;
+  // sweep workspace (grown on demand)
+  mutable DevBuf<double> wa_, wx0_, wx1_, wstate_, wy_;
+  mutable DevBuf<double2> ws0_, ws1_;
+  mutable int work_nvec_ = 0;
+};
+
+}  // namespace sdv

@@ -1,0 +1,38 @@
+// Device linear-algebra primitives for the sketch / PCG / Woodbury layer.
+// All reductions are deterministic (fixed grid, fixed-order tree).
+#pragma once
+
+#include "common.cuh"
+
+namespace sdv {
+
+// Number of kernel launches issued by this library (for bench gpu_launches).
+extern unsigned long long g_launches;
+inline void count_launch(unsigned long long k = 1) { g_launches += k; }
+
+// out[0] = sum_i a[i] * b[i] (device scalar), deterministic.
+void dev_dot(const double* a, const double* b, long long n, double* out, cudaStream_t st);
+// Column dots: out[j] = sum_i a[i + j*lda] * b[i + j*ldb], j < ncols.
+void dev_coldots(const double* a, long long lda, const double* b, long long ldb, long long n, int ncols, double* out,
+                 cudaStream_t st);
+// y = alpha x + beta y   (alpha/beta host scalars)
+void dev_axpby(long long n, double alpha, const double* x, double beta, double* y, cudaStream_t st);
+// y = alpha x + beta y with alpha = (*num / *den) * sa (device scalars), used by PCG without host sync.
+void dev_scale_copy(long long n, double a, const double* x, double* y, cudaStream_t st);
+void dev_fill(long long n, double v, double* y, cudaStream_t st);
+// C (k x l) = A^T B with A (n x k), B (n x l) column-major, leading dims n. Deterministic.
+void dev_gemm_tn(long long n, int k, int l, const double* a, const double* b, double* c, cudaStream_t st);
+// C (n x l) = alpha * A (n x k) * B (k x l) + beta * C; B small, device, column-major (ldb = k).
+void dev_gemm_nn_small(long long n, int k, int l, double alpha, const double* a, const double* b, double beta,
+                       double* c, cudaStream_t st);
+// Row-wise lower-triangular solve: for every row r of Y (n x l), x = L^{-1} y_r,
+// stored as row r of X (n x l). L is l x l lower (device, column-major).
+void dev_trsm_rows_lower(long long n, int l, const double* lmat, const double* y, double* x, cudaStream_t st);
+
+// Householder thin QR on the device (same arithmetic as the reference's
+// Eigen HouseholderQR + sign fix, proj/src/linalg.cpp:108-134).
+// y (n x l) is overwritten by Q; r_host receives R (l x l, column-major).
+// Returns the number of deficient columns.
+int dev_householder_qr(long long n, int l, double* y, double* r_host, cudaStream_t st);
+
+}  // namespace sdv

@@ -72,8 +72,9 @@ def gaussian_matrix(n, l, seed):
 class Scenario:
     """Oracle scenario for BASELINE config 0..4 (or 100 = burgers_1_1)."""
 
-    def __init__(self, cfg):
-        self.h = _chk(lib().oracle_scenario_create(cfg))
+    def __init__(self, cfg, steps=-1, spi=-1):
+        self.cfg = cfg
+        self.h = _chk(lib().oracle_scenario_create_ex(cfg, steps, spi))
         info = np.zeros(4, np.int64)
         _chk(lib().oracle_scenario_info(self.h, info.ctypes.data_as(I64)))
         self.n, self.n_obs, self.n_t, self.spi = (int(x) for x in info)

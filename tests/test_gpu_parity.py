@@ -1,0 +1,174 @@
+"""GPU parity: the sm_100a CUDA path (through the C-ABI) against the CPU
+oracle on the same seeded inputs. Tolerances are the north star's:
+Hessian products 1e-10 relative l2, sketch eigenvalues 1e-8 relative,
+PCG iteration counts +-1 per GN step, final analysis 1e-8 relative.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+# (config, steps, spi): full grids; long windows shortened where the oracle
+# would take minutes (C3 at 512^2 keeps 2 intervals of 8 steps).
+CASES = [(0, -1, -1), (1, -1, -1), (2, -1, -1), (4, 40, -1), (3, 16, 8)]
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def pair(oracle, cfg, steps=-1, spi=-1, block_group=0):
+    from paper_2401_15758_b200 import scenario
+
+    osc = oracle.Scenario(cfg, steps=steps, spi=spi)
+    prob = scenario.from_arrays(scenario.CONFIGS[cfg], osc.indices, osc.values, osc.variances, osc.background,
+                                block_group=block_group, steps=steps, spi=spi)
+    assert (prob.n, prob.m, prob.n_t, prob.spi) == (osc.n, osc.m, osc.n_t, osc.spi)
+    return osc, prob
+
+
+@pytest.mark.parametrize("cfg,steps,spi", CASES)
+def test_prior_sqrt_parity(oracle, sdv, cfg, steps, spi):
+    osc, prob = pair(oracle, cfg, steps, spi)
+    V = oracle.gaussian_matrix(osc.n, 3, 21)
+    G = prob.prior_sqrt(V)
+    for j in range(3):
+        assert rel(G[j], osc.prior_sqrt(V[j])) <= 1e-12
+
+
+@pytest.mark.parametrize("cfg,steps,spi", CASES)
+def test_linearize_states_parity(oracle, sdv, cfg, steps, spi):
+    osc, prob = pair(oracle, cfg, steps, spi)
+    otr = osc.linearize(osc.background)
+    gtr = prob.linearize(osc.background)
+    for i in range(1, osc.n_t + 1):
+        st = i * osc.spi
+        assert rel(gtr.state_at(st), otr.state_at(st)) <= 1e-11, i
+
+
+@pytest.mark.parametrize("cfg,steps,spi", CASES)
+def test_misfit_block_parity_and_dot(oracle, sdv, cfg, steps, spi):
+    """Block TLM (A V) and ADJ (A^T W) vs oracle <= 1e-10; GPU dot test <= 1e-10."""
+    osc, prob = pair(oracle, cfg, steps, spi)
+    otr = osc.linearize(osc.background)
+    gtr = prob.linearize(osc.background)
+    s = 3
+    V = oracle.gaussian_matrix(osc.n, s, 11)
+    W = oracle.gaussian_matrix(osc.m, s, 12)
+    Yg, Zg = gtr.misfit_apply(V), gtr.misfit_adjoint(W)
+    Yo, Zo = otr.misfit_apply(V, workers=8), otr.misfit_adjoint(W, workers=8)
+    for j in range(s):
+        assert rel(Yg[j], Yo[j]) <= 1e-10, ("Y", j)
+        assert rel(Zg[j], Zo[j]) <= 1e-10, ("Z", j)
+        assert abs(Yg[j] @ W[j] - V[j] @ Zg[j]) <= 1e-10 * np.linalg.norm(V[j]) * np.linalg.norm(W[j])
+    HV = gtr.gram(V)
+    for j in range(s):
+        assert rel(HV[j], Zo[j] * 0 + otr.misfit_adjoint(Yo[j:j + 1])[0]) <= 1e-10
+
+
+@pytest.mark.parametrize("cfg,steps,spi", [(0, -1, -1), (2, 40, -1)])
+def test_tlm_adj_range_parity(oracle, sdv, cfg, steps, spi):
+    """LinearizedTrajectory::tlm_range/adj_range on sub-ranges (proj/tests/test_burgers.cpp:147-156)."""
+    osc, prob = pair(oracle, cfg, steps, spi)
+    otr = osc.linearize(osc.background)
+    gtr = prob.linearize(osc.background)
+    x = oracle.gaussian_matrix(osc.n, 1, 5)[0]
+    T = osc.n_t * osc.spi
+    for b, e in [(0, T), (3, 7), (T // 2, T)]:
+        assert rel(gtr.tlm_range(b, e, x)[0], otr.tlm_range(b, e, x)) <= 1e-10
+        assert rel(gtr.adj_range(b, e, x)[0], otr.adj_range(b, e, x)) <= 1e-10
+    # segmented adjoint composition
+    full = gtr.adj_range(0, T, x)[0]
+    seg = gtr.adj_range(0, T // 2, gtr.adj_range(T // 2, T, x))[0]
+    assert rel(seg, full) <= 1e-13
+
+
+@pytest.mark.parametrize("cfg,steps,spi", [(0, -1, -1), (1, -1, -1), (2, 40, -1)])
+def test_evaluate_parity(oracle, sdv, cfg, steps, spi):
+    osc, prob = pair(oracle, cfg, steps, spi)
+    z = 0.01 * oracle.gaussian_matrix(osc.n, 1, 3)[0]
+    x = osc.background + osc.prior_sqrt(z)
+    co, go, lo, _ = osc.evaluate(x, z)
+    cg, gg, lg = prob.evaluate(x, z)
+    assert abs(cg - co) <= 1e-12 * abs(co)
+    assert rel(gg, go) <= 1e-10
+    assert rel(lg, lo) <= 1e-10
+
+
+def test_device_householder_qr_parity(oracle, sdv):
+    osc, prob = pair(oracle, 0)
+    rng = np.random.default_rng(7)
+    y = rng.standard_normal((5000, 40)) @ np.diag(np.logspace(0, -6, 40))
+    qg, rg, ndg = prob.thin_qr(y)
+    qo, ro, ndo = oracle.thin_qr(y)
+    assert ndg == ndo == 0
+    assert np.all(np.diag(rg) >= 0)
+    assert rel(rg, ro) <= 1e-12
+    assert rel(qg, qo) <= 1e-9
+    assert np.linalg.norm(qg.T @ qg - np.eye(40)) <= 1e-13
+
+
+def test_woodbury_parity(oracle, sdv):
+    osc, prob = pair(oracle, 0)
+    rng = np.random.default_rng(8)
+    V, _ = np.linalg.qr(rng.standard_normal((osc.n, 12)))
+    lam = np.logspace(3, -3, 12)
+    v = rng.standard_normal((2, osc.n))
+    out = prob.woodbury_apply(V.T, lam, v)
+    for j in range(2):
+        assert rel(out[j], oracle.woodbury(V, lam, v[j])) <= 1e-12
+
+
+def eig_rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("cfg,method,rank", [(0, 0, 30), (0, 1, 30), (0, 2, 20), (0, 3, 12), (2, 1, 50),
+                                             (1, 0, 60)])
+def test_sketch_eigenvalue_parity(oracle, sdv, cfg, method, rank):
+    osc, prob = pair(oracle, cfg)
+    otr = osc.linearize(osc.background)
+    gtr = prob.linearize(osc.background)
+    seed = 123
+    eo, _, co = otr.sketch(method, rank, seed, workers=8)
+    eg, bg, cg = gtr.sketch(method, rank, seed)
+    assert tuple(cg) == tuple(co)
+    assert eig_rel(eg, eo[:len(eg)]) <= 1e-8
+    assert np.linalg.norm(bg @ bg.T - np.eye(len(eg))) <= 1e-8
+
+
+def test_pcg_iterations_parity(oracle, sdv):
+    osc, prob = pair(oracle, 0)
+    gtr = prob.linearize(osc.background)
+    rhs = oracle.gaussian_matrix(osc.n, 1, 31)[0]
+    eig, basis, _ = gtr.sketch(0, 30, 9)
+    x_plain, it_plain, conv = gtr.pcg_solve(rhs, tol=1e-8)
+    x_pre, it_pre, conv2 = gtr.pcg_solve(rhs, basis, eig, tol=1e-8)
+    assert conv and conv2 and it_pre < it_plain
+    # reference solution by the oracle Hessian columns (dense, n = 256)
+    otr = osc.linearize(osc.background)
+    H = otr.gram(np.eye(osc.n), workers=8)
+    xd = np.linalg.solve(np.eye(osc.n) + H, rhs)
+    assert rel(x_plain, xd) <= 1e-7 and rel(x_pre, xd) <= 1e-7
+
+
+@pytest.mark.parametrize("cfg,mode,method", [(0, 1, 0), (0, 1, 1), (0, 1, 2), (0, 3, 0), (0, 0, 0), (0, 2, 1),
+                                             (1, 1, 0)])
+def test_gn_solve_parity(oracle, sdv, cfg, mode, method):
+    """Final analysis <= 1e-8 relative, PCG counts +-1 per GN step, same counters."""
+    osc, prob = pair(oracle, cfg)
+    from paper_2401_15758_b200 import scenario
+
+    kw = scenario.CONFIGS[cfg].gn_kwargs()
+    kw.update(mode=mode, method=method)
+    if mode == 2:
+        kw.update(rank=10, growth=10, max_rank=30, rank2=61)
+    ro = osc.gn_solve(mode=mode, method=method, rank=kw["rank"], rank2=kw.get("rank2", -1), growth=kw["growth"],
+                      max_rank=kw["max_rank"], workers=8)
+    rg = prob.gn_solve(**kw)
+    assert len(rg["log"]) == len(ro["log"])
+    assert np.all(np.abs(rg["log"][:, 4] - ro["log"][:, 4]) <= 1)
+    assert rel(rg["analysis"], ro["analysis"]) <= 1e-8
+    assert np.array_equal(rg["log"][:, 14:16], ro["log"][:, 14:16])
+    if len(ro["eig0"]):
+        assert eig_rel(rg["eig0"], ro["eig0"]) <= 1e-8
