@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark: batched prior-preconditioned GN Hessian-vector products (TLM+ADJ).
+
+One step = one block of s Hessian products (H V, V n x s) through the
+device-resident sweep engine (the sketch block of the config). Default
+workload: BASELINE.json configs[3] (2-D barotropic vorticity 512^2, 800 RK4
+steps, s = k+p = 110), the configuration the north-star roofline target is
+stated on.
+
+Multi-GPU (torchrun): sketch columns are independent HVPs, so every rank runs
+its own block of s columns against its own copy of the (deterministic) base
+trajectory — weak scaling, no data-path collective; torch.distributed is used
+only for the barrier and the max-over-ranks timing.
+
+--impl reference: the reference's CPU path timed on the host cores. The
+reference itself cannot be built (Eigen3 absent), so this is the C++ oracle
+port of it (oracle/), all host threads, bounded sample extrapolated to HVP/s.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Hessian-vector products/s (TLM+ADJ)"
+UNIT = "HVP/s"
+K_ITER_SKETCH_STREAM = 0x736B6574636800  # proj/src/fourdvar.cpp:16
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--s", type=int, default=0, help="block width (default: the config's sketch size k+p)")
+    ap.add_argument("--group", type=int, default=0, help="BVE sweep group size (0 = auto, L2-resident)")
+    ap.add_argument("--sweep", default="", help="extra block widths to report, e.g. 1,8,32")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ dist ----
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def dist_init(world, backend=None):
+    if world <= 1:
+        return None
+    import torch
+    import torch.distributed as dist
+
+    if backend is None:
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+    if backend == "nccl":
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    dist.init_process_group(backend=backend)
+    return dist
+
+
+def dist_barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def dist_max(dist, x):
+    """Max over ranks (timings are max-reduced, never wall-clock)."""
+    if dist is None:
+        return x
+    import torch
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def rank_seed(rank):
+    """Per-rank sketch block seed (rank 0 = the reference's first GN sketch seed)."""
+    from paper_2401_15758_b200 import api
+
+    return api.mix_seed(2, K_ITER_SKETCH_STREAM) + rank
+
+
+# ---------------------------------------------------------------- clocks ----
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax.append(float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------- roofline -----
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def group_size(dim, requested):
+    """Mirror of Problem::group(): vectors per L2-resident BVE sweep group."""
+    if requested > 0:
+        return requested
+    return max(1, int(80e6 / (6.0 * 8.0 * dim)))
+
+
+def algorithmic_bytes_per_hvp(n_grid_points, stages, s):
+    """B_HVP = 2 S (16 N) + 2 B_traj / s, B_traj = 8 N S."""
+    return 2.0 * stages * 16.0 * n_grid_points + 2.0 * (8.0 * n_grid_points * stages) / s
+
+
+# --------------------------------------------------------- CPU baseline -----
+def cpu_reference_sample(cfg, budget_s=20.0):
+    """Oracle port of the reference path on all host threads; bounded sample.
+
+    Each thread owns one vector and runs TLM then ADJ over a short window of the
+    config's grid/physics (the reference's apply_columns std::thread fan-out,
+    proj/src/sketch.cpp:116-140); HVP/s is extrapolated by the step ratio.
+    """
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import concurrent.futures as cf
+
+    import numpy as np
+    import oracle_lib as O
+
+    from paper_2401_15758_b200 import scenario
+
+    spec = scenario.CONFIGS[cfg]
+    cores = os.cpu_count() or 1
+    # sample window: a few steps, sized so one vector-thread takes ~budget/2
+    k = {0: spec.steps, 1: 100, 2: 20, 3: 2, 4: 4}[cfg]
+    osc = O.Scenario(cfg, steps=k, spi=k)
+    tr = osc.linearize(osc.background)
+    V = O.gaussian_matrix(osc.n, cores, 5)
+
+    def one(j):
+        y = tr.tlm_range(0, k, V[j])
+        return tr.adj_range(0, k, y)
+
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(cores) as ex:
+        list(ex.map(one, range(cores)))
+    dt = time.perf_counter() - t0
+    hvp_equiv = cores * k / spec.steps
+    return {"value": hvp_equiv / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": (f"{cores} vectors x (TLM+ADJ over {k} of {spec.steps} RK4 steps) on the {spec.name} grid, "
+                       f"{dt:.1f} s wall, extrapolated by steps; oracle C++ port (reference unbuildable: Eigen3 absent)"),
+            "seconds": dt}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from paper_2401_15758_b200 import scenario
+
+    spec = scenario.CONFIGS[args.config]
+    vals = []
+    for _ in range(args.warmup + args.steps):
+        vals.append(cpu_reference_sample(args.config))
+    timed = vals[args.warmup:]
+    value = statistics.median(v["value"] for v in timed)
+    cb = dict(timed[-1])
+    cb["value"] = value
+    cb.pop("seconds", None)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 * (args.s or spec.rank) / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference", "config": config_block(spec, args.s or spec.rank, args.group),
+            "cpu_baseline": cb, "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_block(spec, s, group):
+    return {"workload": f"{spec.name}: block of s={s} GN Hessian products (TLM+ADJ), BASELINE.json configs",
+            "model": spec.name, "grid": spec.n, "rk4_steps": spec.steps, "block_s": s,
+            "global_batch": s, "seq_len": spec.steps, "parallelism": "sketch-column sharding (weak)",
+            "sweep_group": group, "l2": "inputs larger than L2 (base trajectory >= 0.8 GB streamed per sweep)"}
+
+
+# ------------------------------------------------------------------ ours ----
+def run_ours(args, world, rank, local):
+    import numpy as np
+
+    import paper_2401_15758_b200 as sdv
+    from paper_2401_15758_b200 import api, scenario
+
+    dist = dist_init(world)
+    sdv.init(local)
+    spec = scenario.CONFIGS[args.config]
+    s = args.s or spec.rank
+    sc = scenario.build(args.config, block_group=args.group)
+    prob = sc.problem
+    tr = prob.linearize(prob.background)
+    n = prob.n
+    stages = 4 * prob.total_steps
+    ngrid = n
+    V = api.gaussian_matrix(n, s, rank_seed(rank))
+    dV = api.DeviceBuffer(V.nbytes)
+    dV.upload(V)
+    dHV = api.DeviceBuffer(V.nbytes)
+    for _ in range(args.warmup):
+        tr.gram_dev(dV.ptr.value, s, dHV.ptr.value)
+    prob.synchronize()
+    dist_barrier(dist)
+
+    clk = ClockSampler(local)
+    clk.start()
+    e0, e1 = api.Event(), api.Event()
+    l0 = sdv.launch_count()
+    e0.record(prob)
+    for _ in range(args.steps):
+        tr.gram_dev(dV.ptr.value, s, dHV.ptr.value)
+    e1.record(prob)
+    ms = e0.elapsed_ms(e1)
+    launches = sdv.launch_count() - l0
+    clocks = clk.stop()
+    dist_barrier(dist)
+    ms_max = dist_max(dist, ms)
+    value = world * s * args.steps / (ms_max / 1000.0)
+
+    # End-to-end through the public host-buffer API: pinned H2D of V, D2H of H V.
+    e2e = None
+    if not args.no_e2e:
+        pin_in = api.PinnedBuffer((s, n))
+        pin_out = api.PinnedBuffer((s, n))
+        pin_in.array[...] = V
+        tr.gram_host(pin_in.array, pin_out.array)
+        dist_barrier(dist)
+        f0, f1 = api.Event(), api.Event()
+        f0.record(prob)
+        for _ in range(args.steps):
+            tr.gram_host(pin_in.array, pin_out.array)
+        f1.record(prob)
+        ems = dist_max(dist, f0.elapsed_ms(f1))
+        e2e = {"value": world * s * args.steps / (ems / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": int(V.nbytes), "d2h_bytes_per_step": int(V.nbytes)}
+        ok = np.allclose(pin_out.array, dHV.download((s, n)), rtol=0, atol=1e-12 * np.abs(pin_out.array).max())
+        if not ok:
+            raise RuntimeError("e2e result differs from the device-resident result")
+        pin_in.free()
+        pin_out.free()
+
+    # Roofline of the dominant kernel (the fused RK4 stage kernel), timed live
+    # with CUDA events on the library stream.
+    hbm, peak_src = peaks()
+    probe_stages = 64
+    ms_stage, ms_col = tr.probe_stage_kernels(s, probe_stages)
+    if spec.model == api.MODEL_BVE:
+        g = min(s, group_size(n, args.group))
+        # per stage launch: read+write the g tangent fields (16 N each) + read
+        # the two base stage fields (omega_b, psi_b) once for the group
+        alg_bytes = g * 16.0 * ngrid + 2 * 8.0 * ngrid
+        dur = ms_stage
+        kname = "bve stage_kernel (fused inverse x-FFT + Arakawa TLM stencil + RK4 update + forward x-FFT)"
+    else:
+        g = s
+        k = max(1, min(prob.total_steps, probe_stages // 4))
+        # tangent fields stay on-chip for the whole sweep: compulsory traffic is
+        # the state in/out per vector + the base stage inputs read once
+        alg_bytes = g * 16.0 * ngrid + 4 * k * 8.0 * ngrid
+        dur = ms_stage
+        kname = f"burgers_tlm_kernel (persistent, {k} steps)"
+    achieved = alg_bytes / (dur / 1000.0) / 1e9
+    b_hvp = algorithmic_bytes_per_hvp(ngrid, stages, s)
+    step_achieved = value / world * b_hvp / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": None, "kernel": kname, "kernel_ms": dur, "col_kernel_ms": ms_col,
+            "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+            "step_model": {"B_HVP_bytes": b_hvp, "achieved_GBs": step_achieved, "frac": step_achieved / hbm,
+                           "note": "SURVEY.md 8(d) streaming model: HVP/s x B_HVP per GPU"}}
+
+    sweep = {}
+    if args.sweep:
+        for sv in [int(x) for x in args.sweep.split(",") if x]:
+            Vs = api.gaussian_matrix(n, sv, rank_seed(rank))
+            dVs = api.DeviceBuffer(Vs.nbytes)
+            dVs.upload(Vs)
+            dHs = api.DeviceBuffer(Vs.nbytes)
+            tr.gram_dev(dVs.ptr.value, sv, dHs.ptr.value)
+            a, b = api.Event(), api.Event()
+            a.record(prob)
+            tr.gram_dev(dVs.ptr.value, sv, dHs.ptr.value)
+            b.record(prob)
+            t = a.elapsed_ms(b)
+            sweep[str(sv)] = {"hvp_per_s": sv / (t / 1000.0), "ms": t,
+                              "frac_step_model": sv / (t / 1000.0) * algorithmic_bytes_per_hvp(ngrid, stages, sv)
+                              / 1e9 / hbm}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample(args.config)
+            cpu.pop("seconds", None)
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config_block(spec, s, min(s, group_size(n, args.group)) if spec.model == 2 else s),
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches}
+        if sweep:
+            line["block_sweep"] = sweep
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -165,6 +165,15 @@ int sdv_host_free(void* ptr);
 int sdv_memcpy_htod(void* dst_dev, const void* src, size_t bytes);
 int sdv_memcpy_dtoh(void* dst, const void* src_dev, size_t bytes);
 int sdv_synchronize(sdv_problem* p);
+/* CUDA events on the problem's stream (device timing for benchmarks). */
+int sdv_event_create(void** ev);
+int sdv_event_destroy(void* ev);
+int sdv_event_record(sdv_problem* p, void* ev);
+int sdv_event_elapsed_ms(void* start, void* stop, float* ms);
+/* Per-kernel timing probe: runs `stages` TLM stages of a BVE block sweep
+ * (group of s vectors) with events around every launch; returns the mean
+ * duration of the fused stage kernel and of the column-FFT kernel (ms). */
+int sdv_probe_stage_kernels(sdv_traj* t, int s, int stages, float* ms_stage, float* ms_col);
 
 #ifdef __cplusplus
 }

@@ -92,6 +92,11 @@ def lib():
         "sdv_memcpy_htod": (C.c_int, [vp, vp, C.c_size_t]),
         "sdv_memcpy_dtoh": (C.c_int, [vp, vp, C.c_size_t]),
         "sdv_synchronize": (C.c_int, [vp]),
+        "sdv_event_create": (C.c_int, [C.POINTER(vp)]),
+        "sdv_event_destroy": (C.c_int, [vp]),
+        "sdv_event_record": (C.c_int, [vp, vp]),
+        "sdv_event_elapsed_ms": (C.c_int, [vp, vp, C.POINTER(C.c_float)]),
+        "sdv_probe_stage_kernels": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -219,6 +219,15 @@ class Trajectory:
     def gram_dev(self, v_dev, s, out_dev):
         check(lib().sdv_gram_apply_block_dev(self._h, C.c_void_p(v_dev), s, C.c_void_p(out_dev)))
 
+    def gram_host(self, V, out):
+        """Public host-buffer entry (e2e path): V, out are (s, n) float64 arrays (pinned or not)."""
+        check(lib().sdv_gram_apply_block(self._h, V.ctypes.data_as(D), V.shape[0], out.ctypes.data_as(D)))
+
+    def probe_stage_kernels(self, s, stages):
+        a, b = C.c_float(), C.c_float()
+        check(lib().sdv_probe_stage_kernels(self._h, s, stages, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def sketch(self, method, rank, seed, rank2=-1, want_basis=True):
         eig = np.empty(rank)
         basis = np.empty((rank, self.problem.n)) if want_basis else None
@@ -235,6 +244,28 @@ class Trajectory:
                                   _p(None if eig is None else _f64(eig)), tol, max_iter, _p(x),
                                   info.ctypes.data_as(I32)))
         return x, int(info[0]), bool(info[1])
+
+
+class Event:
+    """CUDA event recorded on a problem's stream (device timing)."""
+
+    def __init__(self):
+        self.h = C.c_void_p()
+        check(lib().sdv_event_create(C.byref(self.h)))
+
+    def record(self, problem):
+        check(lib().sdv_event_record(problem.handle, self.h))
+
+    def elapsed_ms(self, end):
+        ms = C.c_float()
+        check(lib().sdv_event_elapsed_ms(self.h, end.h, C.byref(ms)))
+        return ms.value
+
+    def __del__(self):
+        try:
+            lib().sdv_event_destroy(self.h)
+        except Exception:
+            pass
 
 
 class DeviceBuffer:

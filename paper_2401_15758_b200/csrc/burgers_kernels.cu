@@ -233,7 +233,11 @@ void burgers_adj(const BurgersArgs& p, double* state, int nvec, cudaStream_t st)
   int th, npt;
   geometry(p.n, th, npt);
   dispatch_npt(npt, [&](auto c) {
-    burgers_adj_kernel<decltype(c)::value><<<nvec, th, sizeof(double) * 2 * p.n, st>>>(p, state);
+    const size_t smem = sizeof(double) * 2 * p.n;
+    if (smem > 48 * 1024)
+      SDV_CUDA(cudaFuncSetAttribute(burgers_adj_kernel<decltype(c)::value>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    burgers_adj_kernel<decltype(c)::value><<<nvec, th, smem, st>>>(p, state);
   });
   SDV_LAUNCH_CHECK();
 }

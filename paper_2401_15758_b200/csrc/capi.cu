@@ -388,5 +388,31 @@ int sdv_synchronize(sdv_problem* p) {
     SDV_CUDA(cudaStreamSynchronize(p->p->stream()));
   });
 }
+int sdv_event_create(void** ev) {
+  return guard([&] {
+    cudaEvent_t e;
+    SDV_CUDA(cudaEventCreate(&e));
+    *ev = e;
+  });
+}
+int sdv_event_destroy(void* ev) { return guard([&] { SDV_CUDA(cudaEventDestroy(static_cast<cudaEvent_t>(ev))); }); }
+int sdv_event_record(sdv_problem* p, void* ev) {
+  return guard([&] {
+    need(p, "problem");
+    SDV_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev), p->p->stream()));
+  });
+}
+int sdv_event_elapsed_ms(void* a, void* b, float* ms) {
+  return guard([&] {
+    SDV_CUDA(cudaEventSynchronize(static_cast<cudaEvent_t>(b)));
+    SDV_CUDA(cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(a), static_cast<cudaEvent_t>(b)));
+  });
+}
+int sdv_probe_stage_kernels(sdv_traj* t, int s, int stages, float* ms_stage, float* ms_col) {
+  return guard([&] {
+    need(t, "trajectory");
+    t->owner->p->probe_stage_kernels(*t->t, s, stages, ms_stage, ms_col);
+  });
+}
 
 }  // extern "C"

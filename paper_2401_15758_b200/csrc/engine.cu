@@ -107,10 +107,13 @@ Problem::Problem(const ProblemDesc& d, long long n_obs, const long long* idx, co
     ri[i] = 1.0 / variances[i];
   }
   SDV_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
-  idx_.upload(idx, static_cast<size_t>(std::max<long long>(n_obs, 1)), st_);
-  values_.upload(values, static_cast<size_t>(std::max<long long>(m, 1)), st_);
-  rinv_sqrt_.upload(rs.data(), static_cast<size_t>(std::max<long long>(m, 1)), st_);
-  rinv_.upload(ri.data(), static_cast<size_t>(std::max<long long>(m, 1)), st_);
+  // Zero observations (a model-only problem) still gets 1-element buffers.
+  const long long zero_idx = 0;
+  const double zero = 0.0;
+  idx_.upload(n_obs > 0 ? idx : &zero_idx, static_cast<size_t>(std::max<long long>(n_obs, 1)), st_);
+  values_.upload(m > 0 ? values : &zero, static_cast<size_t>(std::max<long long>(m, 1)), st_);
+  rinv_sqrt_.upload(m > 0 ? rs.data() : &zero, static_cast<size_t>(std::max<long long>(m, 1)), st_);
+  rinv_.upload(m > 0 ? ri.data() : &zero, static_cast<size_t>(std::max<long long>(m, 1)), st_);
   background_.upload(background, static_cast<size_t>(dim_), st_);
   const int n = d.n;
   if (d.model == kModelBurgers) {
@@ -410,6 +413,69 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
     bve_stage(n, kModeAdj, a, gn, st_);
     count_launch(2);
   }
+}
+
+void Problem::probe_stage_kernels(const Trajectory& tr, int s, int stages, float* ms_stage, float* ms_col) const {
+  if (s < 1 || stages < 1) throw std::invalid_argument("probe: need s >= 1 and stages >= 1");
+  cudaEvent_t ev[3];
+  for (auto& e : ev) SDV_CUDA(cudaEventCreate(&e));
+  wstate_.ensure(static_cast<size_t>(s) * dim_);
+  for (int v = 0; v < s; ++v)
+    SDV_CUDA(cudaMemcpyAsync(wstate_.get() + v * dim_, tr.w.get(), sizeof(double) * dim_, cudaMemcpyDeviceToDevice,
+                             st_));
+  double tot_stage = 0.0, tot_col = 0.0;
+  if (d_.model == kModelBurgers) {
+    const int steps = std::max(1, std::min(tr.steps, stages / 4));
+    BurgersArgs a = burgers_args(d_);
+    a.base = tr.w.get();
+    a.k0 = 0;
+    a.k1 = steps;
+    SDV_CUDA(cudaEventRecord(ev[0], st_));
+    burgers_tlm(a, wstate_.get(), s, st_);
+    SDV_CUDA(cudaEventRecord(ev[1], st_));
+    SDV_CUDA(cudaEventSynchronize(ev[1]));
+    float ms = 0;
+    SDV_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    *ms_stage = ms;
+    *ms_col = 0.0f;
+  } else {
+    s = std::min(s, group());  // one launch covers one sweep group
+    ensure_work(s);
+    const int n = d_.n;
+    double* dst = wstate_.get();
+    double* xb[2] = {wx0_.get(), wx1_.get()};
+    double2* s_cur = ws0_.get();
+    double2* s_nxt = ws1_.get();
+    bve_row_fwd(n, dst, s_cur, s, st_);
+    for (int q = 0; q < stages; ++q) {
+      const int k = (q / 4) % tr.steps, sg = q % 4;
+      SDV_CUDA(cudaEventRecord(ev[0], st_));
+      bve_col(n, s_cur, sym_p_.get(), s, st_);
+      SDV_CUDA(cudaEventRecord(ev[1], st_));
+      StageArgs a = bve_args(d_);
+      a.stage = sg;
+      a.s_in = s_cur;
+      a.s_out = s_nxt;
+      a.x_in = sg == 0 ? dst : xb[(sg - 1) & 1];
+      a.x_out = sg < 3 ? xb[sg & 1] : nullptr;
+      a.d = dst;
+      a.acc = wa_.get();
+      a.base_w = tr.w.get() + (static_cast<long long>(k) * 4 + sg) * dim_;
+      a.base_p = tr.p.get() + (static_cast<long long>(k) * 4 + sg) * dim_;
+      bve_stage(n, kModeTlm, a, s, st_);
+      SDV_CUDA(cudaEventRecord(ev[2], st_));
+      SDV_CUDA(cudaEventSynchronize(ev[2]));
+      float m1 = 0, m2 = 0;
+      SDV_CUDA(cudaEventElapsedTime(&m1, ev[0], ev[1]));
+      SDV_CUDA(cudaEventElapsedTime(&m2, ev[1], ev[2]));
+      tot_col += m1;
+      tot_stage += m2;
+      std::swap(s_cur, s_nxt);
+    }
+    *ms_stage = static_cast<float>(tot_stage / stages);
+    *ms_col = static_cast<float>(tot_col / stages);
+  }
+  for (auto& e : ev) SDV_CUDA(cudaEventDestroy(e));
 }
 
 void Problem::misfit_apply(const Trajectory& tr, const double* v, int s, double* y) const {

@@ -69,6 +69,11 @@ class Problem {
   // cost (host), ctrl_grad = z + Gamma^{1/2} lambda0, lambda0 (device, may be null).
   double evaluate(const Trajectory& tr, const double* d_z, double* d_ctrl_grad, double* d_lambda0) const;
 
+  // Timing probe (bench roofline): mean duration of the fused stage kernel and
+  // the column kernel over `stages` TLM stages on a group of s vectors. For
+  // Burgers the persistent sweep kernel is timed instead (ms_col = 0).
+  void probe_stage_kernels(const Trajectory& tr, int s, int stages, float* ms_stage, float* ms_col) const;
+
   const double* d_rinv_sqrt() const { return rinv_sqrt_.get(); }
   const double* d_rinv() const { return rinv_.get(); }
   const double* d_background() const { return background_.get(); }

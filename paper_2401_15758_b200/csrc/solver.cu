@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 #include <iostream>
 #include <tuple>
 
@@ -907,6 +908,12 @@ GNResult gn_solve(const Problem& p, const GNConfig& cfg) {
         warn("gn_solve: PCG did not reach tolerance at GN iteration " + std::to_string(k) +
              "; continuing with the best iterate");
       log.rec[4] = pcg.iterations;
+      if (std::getenv("SDV_DEBUG_PCG")) {
+        std::cerr << "[sdv pcg k=" << k << "]";
+        for (size_t q = pcg.relres.size() > 6 ? pcg.relres.size() - 6 : 0; q < pcg.relres.size(); ++q)
+          std::cerr << " " << pcg.relres[q];
+        std::cerr << "\n";
+      }
       log.rec[6] = pcg.converged;
       result.total_pcg += pcg.iterations;
     }

@@ -167,7 +167,12 @@ def test_gn_solve_parity(oracle, sdv, cfg, mode, method):
                       max_rank=kw["max_rank"], workers=8)
     rg = prob.gn_solve(**kw)
     assert len(rg["log"]) == len(ro["log"])
-    assert np.all(np.abs(rg["log"][:, 4] - ro["log"][:, 4]) <= 1)
+    # +-1 PCG iterations per GN step for the sketch-preconditioned modes. The
+    # unpreconditioned PrecGamma CG (~45 iterations, relres jumping by 10^2
+    # per step near tol) is roundoff-sensitive beyond that: two builds of the
+    # oracle itself (-O2 vs -O0, i.e. with/without FMA contraction) differ by 2.
+    slack = 2 if mode == 3 else 1
+    assert np.all(np.abs(rg["log"][:, 4] - ro["log"][:, 4]) <= slack)
     assert rel(rg["analysis"], ro["analysis"]) <= 1e-8
     assert np.array_equal(rg["log"][:, 14:16], ro["log"][:, 14:16])
     if len(ro["eig0"]):
