@@ -174,25 +174,24 @@ __global__ void __launch_bounds__(1024) burgers_adj_kernel(BurgersArgs p, double
 
 // 1-D periodic circulant apply out = Re IFFT(sym .* FFT(in)), one CTA per vector.
 template <int N>
-__global__ void __launch_bounds__(1024) spectral1d_kernel(const double* __restrict__ in, double* __restrict__ out,
+__global__ void __launch_bounds__(N / 8) spectral1d_kernel(const double* __restrict__ in, double* __restrict__ out,
                                                           const double* __restrict__ sym, const double2* __restrict__ tw) {
-  constexpr int kTeam = N / 4 < 1024 ? N / 4 : 1024;
   extern __shared__ double2 sm2[];
-  double2* a = sm2;
-  double2* b = sm2 + N;
   const long long v = blockIdx.x;
   const int t = threadIdx.x;
-  for (int x = t; x < N; x += kTeam) a[x] = make_double2(in[v * N + x], 0.0);
+  const double* src = in + v * N;
+  double* dst = out + v * N;
+  auto ld_real = [&](int i) { return make_double2(src[i], 0.0); };
+  auto st_buf = [&](int i, double2 z) { sm2[fpad(i)] = z; };
+  fft_team<N, false>(sm2, tw, t, true, ld_real, st_buf);
   __syncthreads();
-  double2* z = fft_team<N, false>(a, b, tw, t, kTeam, true);
-  for (int k = t; k < N; k += kTeam) {
-    const double w = sym[k];
-    z[k] = make_double2(w * z[k].x, w * z[k].y);
-  }
-  __syncthreads();
-  double2* o = (z == a) ? b : a;
-  double2* r = fft_team<N, true>(z, o, tw, t, kTeam, true);
-  for (int x = t; x < N; x += kTeam) out[v * N + x] = r[x].x;
+  auto ld_mul = [&](int k) {
+    const double w = __ldg(sym + k);
+    const double2 z = sm2[fpad(k)];
+    return make_double2(w * z.x, w * z.y);
+  };
+  auto st_out = [&](int i, double2 z) { dst[i] = z.x; };
+  fft_team<N, true>(sm2, tw, t, true, ld_mul, st_out);
 }
 
 namespace {
@@ -245,8 +244,8 @@ void burgers_adj(const BurgersArgs& p, double* state, int nvec, cudaStream_t st)
 namespace {
 template <int N>
 void spectral1d_launch(const double* in, double* out, const double* sym, int nvec, cudaStream_t st) {
-  constexpr int kTeam = N / 4 < 1024 ? N / 4 : 1024;
-  const size_t smem = sizeof(double2) * 2 * N;
+  constexpr int kTeam = FftSize<N>::kTeam;
+  const size_t smem = sizeof(double2) * FftSize<N>::kPadded;
   static bool init = false;
   if (!init) {
     SDV_CUDA(cudaFuncSetAttribute(spectral1d_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,

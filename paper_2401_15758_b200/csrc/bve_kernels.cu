@@ -9,7 +9,8 @@
 // Layout in HBM: a block of s fields is [s][n][n] (x fastest, index i + n*j,
 // as the reference, proj/include/sketchdav/bve.hpp:20). "Row spectra" are
 // [s][n][n/2] double2: the x-FFT of each row with the (real) k=0 and k=n/2
-// coefficients packed into element 0 (re = X(0), im = X(n/2)).
+// coefficients packed into element 0 (re = X(0), im = X(n/2)); two real rows
+// are transformed by one complex FFT (z = a + i b).
 //
 // Every RK4 stage is two launches:
 //   col kernel  : y-FFT of the row spectra, spectral multiply, inverse y-FFT;
@@ -17,196 +18,188 @@
 //                 Arakawa/Laplacian stencils with the stored base stage fields,
 //                 the RK4 (TLM/NL) or adjoint-RK4 (ADJ) update, and the forward
 //                 x-FFT of the next stage's Poisson input for the owned rows.
+#include <type_traits>
+
 #include "bve_kernels.cuh"
 #include "fft.cuh"
-
-#include <type_traits>
 
 namespace sdv {
 
 namespace {
 
+constexpr int kThreads = 256;
+
 template <int N>
-struct RowCfg {
-  static constexpr int kThreads = 256;
-  static constexpr int kTeam = N / 4 < kThreads ? N / 4 : kThreads;
-  static constexpr int kTeams = kThreads / kTeam;
+struct Cfg {
+  static constexpr int kTeam = N / 8;                        // threads per FFT
+  static constexpr int kTeams = kThreads / kTeam;            // FFTs in flight per CTA
+  static constexpr int kPad = FftSize<N>::kPadded;           // double2 per FFT buffer
+  static constexpr int kT = 8;                               // owned rows per stage CTA
+  static constexpr int kNCT = N < kThreads ? N : kThreads;   // column threads
+  static constexpr int kRG = kThreads / kNCT;                // row groups
+  static constexpr int kRPG = kT / kRG;                      // rows per group
+  static constexpr int kCPT = N / kNCT;                      // columns per thread
+  static constexpr int kCW = (N / 2) < (kThreads / kTeam) ? (N / 2) : (kThreads / kTeam);  // col-kernel columns
+  static constexpr size_t kFftBytes = sizeof(double2) * kPad * kTeams;
+  static constexpr size_t kTileBytes = sizeof(double) * (kT + 2) * N;
+  static constexpr size_t kXBytes = kTileBytes > kFftBytes ? kTileBytes : kFftBytes;
+  static constexpr size_t kStageSmem = kTileBytes + kXBytes;
+  static constexpr size_t kRowSmem = kFftBytes;
+  static constexpr size_t kColSmem = sizeof(double2) * kPad * kCW;
 };
 
-// Packed half spectra of rows a, b -> full spectrum of z = a + i b.
+// Packed half spectra (ra, rb) of two real rows -> element i of the full
+// spectrum of z = a + i b.
 template <int N>
-__device__ __forceinline__ void unpack_pair(const double2* __restrict__ ra, const double2* __restrict__ rb, double2* z,
-                                            int t, int nt) {
-  for (int k = t; k < N / 2; k += nt) {
-    const double2 a = ra[k], b = rb[k];
-    if (k == 0) {
-      z[0] = make_double2(a.x, b.x);
-      z[N / 2] = make_double2(a.y, b.y);
-    } else {
-      z[k] = make_double2(a.x - b.y, a.y + b.x);
-      z[N - k] = make_double2(a.x + b.y, b.x - a.y);
-    }
+__device__ __forceinline__ double2 unpack_elem(const double2* __restrict__ ra, const double2* __restrict__ rb, int i) {
+  if (i == 0) return make_double2(ra[0].x, rb[0].x);
+  if (i == N / 2) return make_double2(ra[0].y, rb[0].y);
+  if (i < N / 2) {
+    const double2 a = ra[i], b = rb[i];
+    return make_double2(a.x - b.y, a.y + b.x);
   }
+  const double2 a = ra[N - i], b = rb[N - i];
+  return make_double2(a.x + b.y, b.x - a.y);
 }
-// Full spectrum Z of z = a + i b -> packed half spectra of a and b.
+// Full spectrum z (padded smem) -> packed half spectra of the two real rows.
 template <int N>
 __device__ __forceinline__ void pack_pair(const double2* z, double2* __restrict__ ra, double2* __restrict__ rb, int t,
                                           int nt) {
   for (int k = t; k < N / 2; k += nt) {
     if (k == 0) {
-      const double2 z0 = z[0], zn = z[N / 2];
+      const double2 z0 = z[0], zn = z[fpad(N / 2)];
       ra[0] = make_double2(z0.x, zn.x);
       rb[0] = make_double2(z0.y, zn.y);
     } else {
-      const double2 zk = z[k], zm = z[N - k];
+      const double2 zk = z[fpad(k)], zm = z[fpad(N - k)];
       ra[k] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
       rb[k] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
     }
   }
 }
 
-// Arakawa Jacobian J(a,b) at (x, row r) given 3x3 neighbourhoods
-// a[dy][dx], b[dy][dx] with dy,dx in {0,1,2} <-> offsets {-1,0,+1}.
-// Returns 12 h^2 J (the caller scales).
+// Arakawa Jacobian J(a,b) ~ a_x b_y - a_y b_x from 3x3 neighbourhoods
+// a[dy][dx], b[dy][dx] (dy, dx in {0,1,2} <-> offsets -1, 0, +1); returns 12 h^2 J.
 __device__ __forceinline__ double arakawa12(const double a[3][3], const double b[3][3]) {
-  // J++
   const double jpp = (a[1][2] - a[1][0]) * (b[2][1] - b[0][1]) - (a[2][1] - a[0][1]) * (b[1][2] - b[1][0]);
-  // J+x
   const double jpx = a[1][2] * (b[2][2] - b[0][2]) - a[1][0] * (b[2][0] - b[0][0]) -
                      a[2][1] * (b[2][2] - b[2][0]) + a[0][1] * (b[0][2] - b[0][0]);
-  // Jx+
   const double jxp = b[2][1] * (a[2][2] - a[2][0]) - b[0][1] * (a[0][2] - a[0][0]) -
                      b[1][2] * (a[2][2] - a[0][2]) + b[1][0] * (a[2][0] - a[0][0]);
   return jpp + jpx + jxp;
 }
-
-template <int N>
-__device__ __forceinline__ void load3x3_smem(const double* f, int r, int x, double o[3][3]) {
-#pragma unroll
-  for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-    for (int dx = 0; dx < 3; ++dx) o[dy][dx] = f[(r + dy - 1) * N + ((x + dx - 1) & (N - 1))];
+__device__ __forceinline__ double lap5(const double o[3][3]) {
+  return o[1][0] + o[1][2] + o[0][1] + o[2][1] - 4.0 * o[1][1];
 }
-template <int N>
-__device__ __forceinline__ void load3x3_glob(const double* __restrict__ f, int gy, int x, double o[3][3]) {
+__device__ __forceinline__ void shift3(double w[3][3]) {
 #pragma unroll
-  for (int dy = 0; dy < 3; ++dy) {
-    const double* row = f + static_cast<long long>((gy + dy - 1) & (N - 1)) * N;
-#pragma unroll
-    for (int dx = 0; dx < 3; ++dx) o[dy][dx] = __ldg(row + ((x + dx - 1) & (N - 1)));
+  for (int c = 0; c < 3; ++c) {
+    w[0][c] = w[1][c];
+    w[1][c] = w[2][c];
   }
 }
-__device__ __forceinline__ double lap5(const double o[3][3]) { return o[1][0] + o[1][2] + o[0][1] + o[2][1] - 4.0 * o[1][1]; }
 
 }  // namespace
 
 // ---------------------------------------------------------------- row FFTs --
 template <int N>
-__global__ void __launch_bounds__(256) row_fwd_kernel(const double* __restrict__ f, double2* __restrict__ s, const double2* __restrict__ tw) {
-  using C = RowCfg<N>;
+__global__ void __launch_bounds__(kThreads) row_fwd_kernel(const double* __restrict__ f, double2* __restrict__ s,
+                                                           const double2* __restrict__ tw) {
+  using C = Cfg<N>;
   extern __shared__ double2 sm[];
   const int team = threadIdx.x / C::kTeam, t = threadIdx.x % C::kTeam;
   const int pair = blockIdx.x * C::kTeams + team;
   const bool active = pair < N / 2;
   const long long v = blockIdx.y;
-  double2* a = sm + team * 2 * N;
-  double2* b = a + N;
-  if (active) {
-    const double* r0 = f + v * N * N + static_cast<long long>(2 * pair) * N;
-    for (int x = t; x < N; x += C::kTeam) a[x] = make_double2(r0[x], r0[x + N]);
-  }
+  double2* buf = sm + team * C::kPad;
+  const double* r0 = f + v * N * N + static_cast<long long>(2 * pair) * N;
+  auto load = [&](int i) { return make_double2(r0[i], r0[i + N]); };
+  auto store = [&](int i, double2 z) { buf[fpad(i)] = z; };
+  fft_team<N, false>(buf, tw, t, active, load, store);
   __syncthreads();
-  double2* z = fft_team<N, false>(a, b, tw, t, C::kTeam, active);
   if (active) {
     double2* ra = s + v * N * (N / 2) + static_cast<long long>(2 * pair) * (N / 2);
-    pack_pair<N>(z, ra, ra + N / 2, t, C::kTeam);
+    pack_pair<N>(buf, ra, ra + N / 2, t, C::kTeam);
   }
 }
 
 template <int N>
-__global__ void __launch_bounds__(256) row_inv_kernel(const double2* __restrict__ s, double* __restrict__ f, const double2* __restrict__ tw) {
-  using C = RowCfg<N>;
+__global__ void __launch_bounds__(kThreads) row_inv_kernel(const double2* __restrict__ s, double* __restrict__ f,
+                                                           const double2* __restrict__ tw) {
+  using C = Cfg<N>;
   extern __shared__ double2 sm[];
   const int team = threadIdx.x / C::kTeam, t = threadIdx.x % C::kTeam;
   const int pair = blockIdx.x * C::kTeams + team;
   const bool active = pair < N / 2;
   const long long v = blockIdx.y;
-  double2* a = sm + team * 2 * N;
-  double2* b = a + N;
-  if (active) {
-    const double2* ra = s + v * N * (N / 2) + static_cast<long long>(2 * pair) * (N / 2);
-    unpack_pair<N>(ra, ra + N / 2, a, t, C::kTeam);
-  }
-  __syncthreads();
-  double2* z = fft_team<N, true>(a, b, tw, t, C::kTeam, active);
-  if (active) {
-    double* r0 = f + v * N * N + static_cast<long long>(2 * pair) * N;
-    for (int x = t; x < N; x += C::kTeam) {
-      const double2 q = z[x];
-      r0[x] = q.x;
-      r0[x + N] = q.y;
-    }
-  }
+  double2* buf = sm + team * C::kPad;
+  const double2* ra = s + v * N * (N / 2) + static_cast<long long>(2 * pair) * (N / 2);
+  double* r0 = f + v * N * N + static_cast<long long>(2 * pair) * N;
+  auto load = [&](int i) { return unpack_elem<N>(ra, ra + N / 2, i); };
+  auto store = [&](int i, double2 z) {
+    r0[i] = z.x;
+    r0[i + N] = z.y;
+  };
+  fft_team<N, true>(buf, tw, t, active, load, store);
 }
 
 // ------------------------------------------------------------- column pass --
-// y-FFT of CW adjacent kx columns, multiply by sym[kx*N + ky], inverse y-FFT.
+// y-FFT of kCW adjacent kx columns, multiply by sym[kx*N + ky], inverse y-FFT.
 // Column kx = 0 holds X(0) + i X(n/2) per row; both are real-input columns, so
 // the multiplier is applied through the Hermitian split
 //   Z'(ky) = (s0+sN)/2 Z(ky) + (s0-sN)/2 conj(Z(-ky)).
-template <int N, int CW>
-__global__ void __launch_bounds__(CW*(N / 4)) col_kernel(double2* __restrict__ s, const double* __restrict__ sym, const double2* __restrict__ tw) {
-  constexpr int kTeam = N / 4;
-  constexpr int kThreads = CW * kTeam;
+template <int N>
+__global__ void __launch_bounds__(Cfg<N>::kCW*(N / 8)) col_kernel(double2* __restrict__ s,
+                                                                  const double* __restrict__ sym,
+                                                                  const double2* __restrict__ tw) {
+  using C = Cfg<N>;
+  constexpr int kTh = C::kCW * C::kTeam;
   extern __shared__ double2 sm[];
-  const int team = threadIdx.x / kTeam, t = threadIdx.x % kTeam;
-  const int kx0 = blockIdx.x * CW;
+  const int team = threadIdx.x / C::kTeam, t = threadIdx.x % C::kTeam;
+  const int kx0 = blockIdx.x * C::kCW;
   const long long v = blockIdx.y;
   double2* base = s + v * N * (N / 2) + kx0;
-  for (int e = threadIdx.x; e < CW * N; e += kThreads) {
-    const int y = e / CW, c = e % CW;
-    sm[c * 2 * N + y] = base[static_cast<long long>(y) * (N / 2) + c];
+  for (int e = threadIdx.x; e < C::kCW * N; e += kTh) {
+    const int y = e / C::kCW, c = e % C::kCW;
+    sm[c * C::kPad + fpad(y)] = base[static_cast<long long>(y) * (N / 2) + c];
   }
   __syncthreads();
-  double2* a = sm + team * 2 * N;
-  double2* b = a + N;
-  double2* z = fft_team<N, false>(a, b, tw, t, kTeam, true);
-  double2* o = (z == a) ? b : a;
+  double2* buf = sm + team * C::kPad;
+  auto ld_own = [&](int i) { return buf[fpad(i)]; };
+  auto st_own = [&](int i, double2 z) { buf[fpad(i)] = z; };
+  fft_team<N, false>(buf, tw, t, true, ld_own, st_own);
+  __syncthreads();
   const int kx = kx0 + team;
-  if (kx == 0) {
-    const double* s0 = sym;
-    const double* sn = sym + static_cast<long long>(N / 2) * N;
-    for (int ky = t; ky < N; ky += kTeam) {
-      const double p = 0.5 * (__ldg(s0 + ky) + __ldg(sn + ky)), m = 0.5 * (__ldg(s0 + ky) - __ldg(sn + ky));
-      const double2 zk = z[ky], zm = z[(N - ky) & (N - 1)];
-      o[ky] = make_double2(p * zk.x + m * zm.x, p * zk.y - m * zm.y);
-    }
-  } else {
-    const double* sk = sym + static_cast<long long>(kx) * N;
-    for (int ky = t; ky < N; ky += kTeam) {
+  const double* sk = sym + static_cast<long long>(kx) * N;
+  const double* sn = sym + static_cast<long long>(N / 2) * N;
+  auto ld_mul = [&](int ky) {
+    const double2 z = buf[fpad(ky)];
+    if (kx != 0) {
       const double w = __ldg(sk + ky);
-      o[ky] = make_double2(w * z[ky].x, w * z[ky].y);
+      return make_double2(w * z.x, w * z.y);
     }
-  }
+    const double a = __ldg(sk + ky), b = __ldg(sn + ky);
+    const double pp = 0.5 * (a + b), mm = 0.5 * (a - b);
+    const double2 zm = buf[fpad((N - ky) & (N - 1))];
+    return make_double2(pp * z.x + mm * zm.x, pp * z.y - mm * zm.y);
+  };
+  fft_team<N, true>(buf, tw, t, true, ld_mul, st_own);
   __syncthreads();
-  double2* r = fft_team<N, true>(o, z, tw, t, kTeam, true);
-  const int roff = static_cast<int>(r - a);  // 0 or N (same for every team)
-  for (int e = threadIdx.x; e < CW * N; e += kThreads) {
-    const int y = e / CW, c = e % CW;
-    base[static_cast<long long>(y) * (N / 2) + c] = sm[c * 2 * N + roff + y];
+  for (int e = threadIdx.x; e < C::kCW * N; e += kTh) {
+    const int y = e / C::kCW, c = e % C::kCW;
+    base[static_cast<long long>(y) * (N / 2) + c] = sm[c * C::kPad + fpad(y)];
   }
 }
 
 // --------------------------------------------------------- fused RK stage --
-template <int N, int T, int MODE>
-__global__ void __launch_bounds__(256) stage_kernel(StageArgs p) {
-  using C = RowCfg<N>;
-  constexpr int R = T + 2;        // rows incl. halo
-  constexpr int PTS = T * N / 256;  // owned points per thread
+template <int N, int MODE>
+__global__ void __launch_bounds__(kThreads) stage_kernel(StageArgs p) {
+  using C = Cfg<N>;
+  constexpr int T = C::kT, R = T + 2;
   extern __shared__ double smd[];
-  double* P = smd;                // R x N  inverse-FFT field
-  double* X = P + R * N;          // R x N  stencil input
-  double2* F = reinterpret_cast<double2*>(X + R * N);  // kTeams x 2N
+  double* P = smd;                             // R x N inverse-FFT field
+  double* X = P + R * N;                       // R x N stencil input
+  double2* F = reinterpret_cast<double2*>(X);  // FFT buffers alias X
   const int tid = threadIdx.x;
   const int team = tid / C::kTeam, t = tid % C::kTeam;
   const int y0 = blockIdx.x * T;
@@ -214,55 +207,51 @@ __global__ void __launch_bounds__(256) stage_kernel(StageArgs p) {
   const long long off = v * N * N;
   const long long soff = v * N * (N / 2);
   const double2* tw = p.tw;
-  double2* fa = F + team * 2 * N;
-  double2* fb = fa + N;
+  double2* fbuf = F + team * C::kPad;
   const bool has_prev = MODE != kModeAdj || (p.flags & kFlagHasPrev);
   const bool finish = MODE == kModeAdj && (p.flags & kFlagFinish);
 
-  // Phase 1: inverse x-FFT of rows y0-1 .. y0+T (P field).
+  // Phase 1: inverse x-FFT of rows y0-1 .. y0+T -> P.
   if (has_prev) {
     constexpr int kPairs = R / 2;
-    for (int base = 0; base < kPairs; base += C::kTeams) {
-      const int pr = base + team;
+#pragma unroll 1
+    for (int b0 = 0; b0 < kPairs; b0 += C::kTeams) {
+      const int pr = b0 + team;
       const bool act = pr < kPairs;
-      if (act) {
-        const int ga = (y0 - 1 + 2 * pr) & (N - 1), gb = (y0 + 2 * pr) & (N - 1);
-        unpack_pair<N>(p.s_in + soff + static_cast<long long>(ga) * (N / 2),
-                       p.s_in + soff + static_cast<long long>(gb) * (N / 2), fa, t, C::kTeam);
-      }
-      __syncthreads();
-      const double2* z = fft_team<N, true>(fa, fb, tw, t, C::kTeam, act);
-      if (act) {
-        for (int x = t; x < N; x += C::kTeam) {
-          const double2 q = z[x];
-          P[(2 * pr) * N + x] = q.x;
-          P[(2 * pr + 1) * N + x] = q.y;
-        }
-      }
+      const int ga = (y0 - 1 + 2 * pr) & (N - 1), gb = (y0 + 2 * pr) & (N - 1);
+      const double2* ra = p.s_in + soff + static_cast<long long>(ga) * (N / 2);
+      const double2* rb = p.s_in + soff + static_cast<long long>(gb) * (N / 2);
+      double* pa = P + (2 * pr) * N;
+      auto load = [&](int i) { return unpack_elem<N>(ra, rb, i); };
+      auto store = [&](int i, double2 z) {
+        pa[i] = z.x;
+        pa[i + N] = z.y;
+      };
+      fft_team<N, true>(fbuf, tw, t, act, load, store);
       __syncthreads();
     }
   }
 
-  // Phase 2: stencil input rows.
+  // Phase 2: stencil-input rows (overwrite the FFT buffers).
   if (MODE != kModeAdj) {
     const double* xin = p.x_in + off;
-    for (int e = tid; e < R * N; e += 256) {
+    for (int e = tid; e < R * N; e += kThreads) {
       const int r = e / N, x = e % N;
       X[e] = xin[static_cast<long long>((y0 - 1 + r) & (N - 1)) * N + x];
     }
   } else {
     const double dt = p.dt;
-    for (int e = tid; e < R * N; e += 256) {
+    for (int e = tid; e < R * N; e += kThreads) {
       const int r = e / N, x = e % N;
       const int gy = (y0 - 1 + r) & (N - 1);
       const long long g = off + static_cast<long long>(gy) * N + x;
       const bool owned = r >= 1 && r <= T;
       const double mu = has_prev ? p.q_in[g] + P[e] : 0.0;
-      double a;
       if (finish) {
         if (owned) p.d[g] = p.acc[g] + mu;
         continue;
       }
+      double a;
       switch (p.stage) {
         case 3: {
           const double lam = has_prev ? p.acc[g] + mu : p.d[g];
@@ -295,90 +284,124 @@ __global__ void __launch_bounds__(256) stage_kernel(StageArgs p) {
   }
   __syncthreads();
 
-  // Phase 3: stencils + RK update on owned rows.
+  // Phase 3: stencils + RK update on owned rows. Each thread walks kCPT
+  // columns of kRPG rows with a 3x3 sliding window per field (3 new loads per
+  // field per row).
   const double js = p.inv12h2, ls = p.invh2, nu = p.nu, dt = p.dt;
-  double res[PTS];
+  const int xt = tid % C::kNCT, rg = tid / C::kNCT;
+  const int r0 = 1 + rg * C::kRPG;  // first owned smem row of this group
+  double res[C::kCPT][C::kRPG];
 #pragma unroll
-  for (int q = 0; q < PTS; ++q) {
-    const int e = tid + q * 256;
-    const int r = 1 + e / N, x = e % N;
-    const int gy = (y0 + r - 1) & (N - 1);
-    const long long g = off + static_cast<long long>(gy) * N + x;
-    double xs[3][3];
-    load3x3_smem<N>(X, r, x, xs);
-    if (MODE == kModeNl) {
-      double ps[3][3];
-      load3x3_smem<N>(P, r, x, ps);
-      const double kk = arakawa12(ps, xs) * js + nu * lap5(xs) * ls;
-      if (p.store_w) {
-        p.store_w[static_cast<long long>(gy) * N + x] = xs[1][1];
-        p.store_p[static_cast<long long>(gy) * N + x] = ps[1][1];
+  for (int cc = 0; cc < C::kCPT; ++cc) {
+    const int x = xt + cc * C::kNCT;
+    const int xs[3] = {(x - 1) & (N - 1), x, (x + 1) & (N - 1)};
+    double wx[3][3], wp[3][3], bp[3][3], bw[3][3];
+    auto gload = [&](const double* f, int r, double* w) {
+      const double* row = f + static_cast<long long>((y0 + r - 1) & (N - 1)) * N;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) w[c] = __ldg(row + xs[c]);
+    };
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy) {
+      const int r = r0 - 1 + dy;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        wx[dy][c] = X[r * N + xs[c]];
+        if (MODE != kModeAdj) wp[dy][c] = P[r * N + xs[c]];
       }
-      res[q] = kk;
-    } else if (MODE == kModeTlm) {
-      double ps[3][3], bp[3][3], bw[3][3];
-      load3x3_smem<N>(P, r, x, ps);
-      load3x3_glob<N>(p.base_p, gy, x, bp);
-      load3x3_glob<N>(p.base_w, gy, x, bw);
-      res[q] = (arakawa12(bp, xs) + arakawa12(ps, bw)) * js + nu * lap5(xs) * ls;
-    } else {
-      double bp[3][3], bw[3][3];
-      load3x3_glob<N>(p.base_p, gy, x, bp);
-      load3x3_glob<N>(p.base_w, gy, x, bw);
-      p.q_out[g] = -arakawa12(bp, xs) * js + nu * lap5(xs) * ls;
-      res[q] = -arakawa12(xs, bw) * js;
+      if (MODE != kModeNl) {
+        gload(p.base_p, r, bp[dy]);
+        gload(p.base_w, r, bw[dy]);
+      }
     }
-    if (MODE != kModeAdj) {
-      const double kk = res[q];
-      double xn;
-      switch (p.stage) {
-        case 0: {
-          const double d = p.d[g];
-          p.acc[g] = d + dt / 6.0 * kk;
-          xn = d + 0.5 * dt * kk;
-          p.x_out[g] = xn;
-          break;
+#pragma unroll
+    for (int q = 0; q < C::kRPG; ++q) {
+      const int r = r0 + q;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        wx[2][c] = X[(r + 1) * N + xs[c]];
+        if (MODE != kModeAdj) wp[2][c] = P[(r + 1) * N + xs[c]];
+      }
+      if (MODE != kModeNl) {
+        gload(p.base_p, r + 1, bp[2]);
+        gload(p.base_w, r + 1, bw[2]);
+      }
+      const int gy = (y0 + r - 1) & (N - 1);
+      const long long g = off + static_cast<long long>(gy) * N + x;
+      double out;
+      if (MODE == kModeNl) {
+        out = arakawa12(wp, wx) * js + nu * lap5(wx) * ls;
+        if (p.store_w) {
+          p.store_w[static_cast<long long>(gy) * N + x] = wx[1][1];
+          p.store_p[static_cast<long long>(gy) * N + x] = wp[1][1];
         }
-        case 1: {
-          const double d = p.d[g];
-          p.acc[g] += dt / 3.0 * kk;
-          xn = d + 0.5 * dt * kk;
-          p.x_out[g] = xn;
-          break;
-        }
-        case 2: {
-          const double d = p.d[g];
-          p.acc[g] += dt / 3.0 * kk;
-          xn = d + dt * kk;
-          p.x_out[g] = xn;
-          break;
-        }
-        default: {
-          xn = p.acc[g] + dt / 6.0 * kk;
-          p.d[g] = xn;
-          break;
+      } else if (MODE == kModeTlm) {
+        out = (arakawa12(bp, wx) + arakawa12(wp, bw)) * js + nu * lap5(wx) * ls;
+      } else {
+        p.q_out[g] = -arakawa12(bp, wx) * js + nu * lap5(wx) * ls;
+        out = -arakawa12(wx, bw) * js;
+      }
+      if (MODE != kModeAdj) {
+        const double kk = out;
+        switch (p.stage) {
+          case 0: {
+            const double d = p.d[g];
+            p.acc[g] = d + dt / 6.0 * kk;
+            out = d + 0.5 * dt * kk;
+            p.x_out[g] = out;
+            break;
+          }
+          case 1: {
+            const double d = p.d[g];
+            p.acc[g] += dt / 3.0 * kk;
+            out = d + 0.5 * dt * kk;
+            p.x_out[g] = out;
+            break;
+          }
+          case 2: {
+            const double d = p.d[g];
+            p.acc[g] += dt / 3.0 * kk;
+            out = d + dt * kk;
+            p.x_out[g] = out;
+            break;
+          }
+          default: {
+            out = p.acc[g] + dt / 6.0 * kk;
+            p.d[g] = out;
+            break;
+          }
         }
       }
-      res[q] = xn;
+      res[cc][q] = out;
+      shift3(wx);
+      if (MODE != kModeAdj) shift3(wp);
+      if (MODE != kModeNl) {
+        shift3(bp);
+        shift3(bw);
+      }
     }
   }
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < PTS; ++q) P[N + tid + q * 256] = res[q];
+  for (int cc = 0; cc < C::kCPT; ++cc)
+#pragma unroll
+    for (int q = 0; q < C::kRPG; ++q) P[(r0 + q) * N + xt + cc * C::kNCT] = res[cc][q];
   __syncthreads();
 
   // Phase 4: forward x-FFT of the owned rows -> next row spectra.
   constexpr int kOwnPairs = T / 2;
-  for (int base = 0; base < kOwnPairs; base += C::kTeams) {
-    const int pr = base + team;
+#pragma unroll 1
+  for (int b0 = 0; b0 < kOwnPairs; b0 += C::kTeams) {
+    const int pr = b0 + team;
     const bool act = pr < kOwnPairs;
-    if (act)
-      for (int x = t; x < N; x += C::kTeam) fa[x] = make_double2(P[(1 + 2 * pr) * N + x], P[(2 + 2 * pr) * N + x]);
+    const double* pa = P + (1 + 2 * pr) * N;
+    auto load = [&](int i) { return make_double2(pa[i], pa[i + N]); };
+    auto store = [&](int i, double2 z) { fbuf[fpad(i)] = z; };
+    fft_team<N, false>(fbuf, tw, t, act, load, store);
     __syncthreads();
-    const double2* z = fft_team<N, false>(fa, fb, tw, t, C::kTeam, act);
     if (act) {
       double2* ra = p.s_out + soff + static_cast<long long>(y0 + 2 * pr) * (N / 2);
-      pack_pair<N>(z, ra, ra + N / 2, t, C::kTeam);
+      pack_pair<N>(fbuf, ra, ra + N / 2, t, C::kTeam);
     }
     __syncthreads();
   }
@@ -406,53 +429,49 @@ __global__ void scatter_obs_kernel(double* __restrict__ f, long long dim, const 
 namespace {
 template <int N>
 struct Launch {
-  static constexpr int kT = 8;
-  static constexpr int kCW = N >= 256 ? 4 : (N >= 128 ? 8 : 16);
-  static size_t row_smem() { return sizeof(double2) * 2 * N * RowCfg<N>::kTeams; }
-  static size_t stage_smem() { return sizeof(double) * 2 * (kT + 2) * N + row_smem(); }
-  static size_t col_smem() { return sizeof(double2) * 2 * N * kCW; }
+  using C = Cfg<N>;
   static void setup() {
     static bool done = false;
     if (done) return;
-    SDV_CUDA(cudaFuncSetAttribute(stage_kernel<N, kT, kModeTlm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(stage_smem())));
-    SDV_CUDA(cudaFuncSetAttribute(stage_kernel<N, kT, kModeAdj>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(stage_smem())));
-    SDV_CUDA(cudaFuncSetAttribute(stage_kernel<N, kT, kModeNl>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(stage_smem())));
-    SDV_CUDA(cudaFuncSetAttribute(col_kernel<N, kCW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(col_smem())));
+    SDV_CUDA(cudaFuncSetAttribute(stage_kernel<N, kModeTlm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(C::kStageSmem)));
+    SDV_CUDA(cudaFuncSetAttribute(stage_kernel<N, kModeAdj>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(C::kStageSmem)));
+    SDV_CUDA(cudaFuncSetAttribute(stage_kernel<N, kModeNl>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(C::kStageSmem)));
+    SDV_CUDA(cudaFuncSetAttribute(col_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(C::kColSmem)));
     SDV_CUDA(cudaFuncSetAttribute(row_fwd_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(row_smem())));
+                                  static_cast<int>(C::kRowSmem)));
     SDV_CUDA(cudaFuncSetAttribute(row_inv_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(row_smem())));
+                                  static_cast<int>(C::kRowSmem)));
     done = true;
   }
   static void row_fwd(const double* f, double2* s, int nvec, cudaStream_t st) {
     setup();
-    dim3 g(ceil_div(N / 2, RowCfg<N>::kTeams), nvec);
-    row_fwd_kernel<N><<<g, 256, row_smem(), st>>>(f, s, twiddle_table(N));
+    dim3 g(ceil_div(N / 2, C::kTeams), nvec);
+    row_fwd_kernel<N><<<g, kThreads, C::kRowSmem, st>>>(f, s, twiddle_table(N));
     SDV_LAUNCH_CHECK();
   }
   static void row_inv(const double2* s, double* f, int nvec, cudaStream_t st) {
     setup();
-    dim3 g(ceil_div(N / 2, RowCfg<N>::kTeams), nvec);
-    row_inv_kernel<N><<<g, 256, row_smem(), st>>>(s, f, twiddle_table(N));
+    dim3 g(ceil_div(N / 2, C::kTeams), nvec);
+    row_inv_kernel<N><<<g, kThreads, C::kRowSmem, st>>>(s, f, twiddle_table(N));
     SDV_LAUNCH_CHECK();
   }
   static void col(double2* s, const double* sym, int nvec, cudaStream_t st) {
     setup();
-    dim3 g((N / 2) / kCW, nvec);
-    col_kernel<N, kCW><<<g, kCW * (N / 4), col_smem(), st>>>(s, sym, twiddle_table(N));
+    dim3 g((N / 2) / C::kCW, nvec);
+    col_kernel<N><<<g, C::kCW * C::kTeam, C::kColSmem, st>>>(s, sym, twiddle_table(N));
     SDV_LAUNCH_CHECK();
   }
   static void stage(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
     setup();
-    dim3 g(N / kT, nvec);
+    dim3 g(N / C::kT, nvec);
     switch (mode) {
-      case kModeTlm: stage_kernel<N, kT, kModeTlm><<<g, 256, stage_smem(), st>>>(a); break;
-      case kModeAdj: stage_kernel<N, kT, kModeAdj><<<g, 256, stage_smem(), st>>>(a); break;
-      default: stage_kernel<N, kT, kModeNl><<<g, 256, stage_smem(), st>>>(a); break;
+      case kModeTlm: stage_kernel<N, kModeTlm><<<g, kThreads, C::kStageSmem, st>>>(a); break;
+      case kModeAdj: stage_kernel<N, kModeAdj><<<g, kThreads, C::kStageSmem, st>>>(a); break;
+      default: stage_kernel<N, kModeNl><<<g, kThreads, C::kStageSmem, st>>>(a); break;
     }
     SDV_LAUNCH_CHECK();
   }

@@ -1,11 +1,17 @@
 // Hand-written shared-memory FFT building blocks (no cuFFT on the hot path).
 //
-// fft_team<N, INV>: one length-N complex transform per "team" of threads,
-// Stockham autosort formulation (radix-4 passes, one radix-2 pass when log2 N
-// is odd), ping-ponging between two shared-memory buffers. Twiddles come from
-// a per-length table tw[m] = exp(-2 pi i m / N) in global memory (L1 resident).
-// Unnormalised in both directions; the 1/N^d factors are folded into the
-// spectral multipliers (Poisson symbol, B^{1/2} symbol).
+// fft_team<N, INV>: one length-N complex transform per "team" of N/8 threads.
+// Register-blocked Stockham autosort: every thread holds 8 complex values per
+// pass and performs 8/R radix-R butterflies in registers (radix-8 passes,
+// one trailing radix-4 or radix-2 pass when log2 N is not a multiple of 3:
+// 512 = 8*8*8, 256 = 8*8*4, 128 = 8*8*2, 4096 = 8^4). Passes exchange data
+// in place through one padded shared buffer (index i -> i + i/8, which makes
+// the stride-8 Stockham stores bank-conflict free). The first pass reads
+// through a caller functor (e.g. straight from global memory, unpacking
+// packed real spectra) and the last pass writes through one, so a transform
+// costs P-1 shared-memory round trips. Twiddles come from a per-length table
+// tw[m] = exp(-2 pi i m / N) (L1 resident). Unnormalised in both directions;
+// the 1/N^d factors are folded into the spectral multipliers.
 #pragma once
 
 #include "common.cuh"
@@ -13,80 +19,164 @@
 namespace sdv {
 
 __host__ __device__ constexpr int ilog2_c(int n) { return n <= 1 ? 0 : 1 + ilog2_c(n >> 1); }
+__host__ __device__ __forceinline__ int fpad(int i) { return i + (i >> 3); }
+template <int N>
+struct FftSize {
+  static constexpr int kPadded = N + N / 8;  // double2 elements per team buffer
+  static constexpr int kTeam = N / 8;        // threads per transform
+};
 
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 template <bool CONJ>
-__device__ __forceinline__ double2 cmul_tw(double2 a, double2 w) {
+__host__ __device__ __forceinline__ double2 cmul_tw(double2 a, double2 w) {
   if (CONJ) return make_double2(fma(a.x, w.x, a.y * w.y), fma(a.y, w.x, -a.x * w.y));
   return make_double2(fma(a.x, w.x, -a.y * w.y), fma(a.y, w.x, a.x * w.y));
 }
-
-// Radix-4 butterfly; forward uses -i, inverse +i.
+// multiply by -i (forward) or +i (inverse)
 template <bool INV>
-__device__ __forceinline__ void bfly4(double2& v0, double2& v1, double2& v2, double2& v3) {
-  const double2 y0 = cadd(v0, v2), y1 = csub(v0, v2), y2 = cadd(v1, v3);
-  const double2 d = csub(v1, v3);
-  const double2 y3 = INV ? make_double2(-d.y, d.x) : make_double2(d.y, -d.x);
-  v0 = cadd(y0, y2);
-  v2 = csub(y0, y2);
-  v1 = cadd(y1, y3);
-  v3 = csub(y1, y3);
+__host__ __device__ __forceinline__ double2 mul_mi(double2 d) {
+  return INV ? make_double2(-d.y, d.x) : make_double2(d.y, -d.x);
 }
 
-// All threads of the CTA must call this (it synchronises with __syncthreads
-// after every pass). Team thread t in [0, nt) works on the transform held in
-// a[0..N); b is scratch of the same size. Returns the buffer holding the
-// result (a or b).
-template <int N, bool INV>
-__device__ __forceinline__ double2* fft_team(double2* a, double2* b, const double2* __restrict__ tw, int t, int nt,
-                                             bool active) {
-  constexpr int LOG = ilog2_c(N);
-  int ns = 1;
-#pragma unroll
-  for (int pass = 0; pass < LOG / 2; ++pass) {
-    if (active) {
-      for (int j = t; j < N / 4; j += nt) {
-        const int k = j & (ns - 1);
-        double2 v0 = a[j], v1 = a[j + N / 4], v2 = a[j + N / 2], v3 = a[j + 3 * N / 4];
-        if (ns > 1) {
-          const int st = N / (ns * 4);
-          v1 = cmul_tw<INV>(v1, __ldg(tw + k * st));
-          v2 = cmul_tw<INV>(v2, __ldg(tw + 2 * k * st));
-          v3 = cmul_tw<INV>(v3, __ldg(tw + 3 * k * st));
-        }
-        bfly4<INV>(v0, v1, v2, v3);
-        const int base = (j - k) * 4 + k;
-        b[base] = v0;
-        b[base + ns] = v1;
-        b[base + 2 * ns] = v2;
-        b[base + 3 * ns] = v3;
-      }
-    }
-    __syncthreads();
-    double2* tmp = a;
-    a = b;
-    b = tmp;
-    ns *= 4;
-  }
-  if (LOG & 1) {
-    if (active) {
-      for (int j = t; j < N / 2; j += nt) {
-        const int k = j & (ns - 1);
-        double2 v0 = a[j], v1 = a[j + N / 2];
-        if (ns > 1) v1 = cmul_tw<INV>(v1, __ldg(tw + k * (N / (2 * ns))));
-        const int base = (j - k) * 2 + k;
-        b[base] = cadd(v0, v1);
-        b[base + ns] = csub(v0, v1);
-      }
-    }
-    __syncthreads();
-    double2* tmp = a;
-    a = b;
-    b = tmp;
-  }
-  return a;
+// In-register natural-order DFTs.
+template <bool INV>
+__host__ __device__ __forceinline__ void dft2(double2* v) {
+  const double2 a = v[0], b = v[1];
+  v[0] = cadd(a, b);
+  v[1] = csub(a, b);
 }
+template <bool INV>
+__host__ __device__ __forceinline__ void dft4(double2* v) {
+  const double2 y0 = cadd(v[0], v[2]), y1 = csub(v[0], v[2]), y2 = cadd(v[1], v[3]);
+  const double2 y3 = mul_mi<INV>(csub(v[1], v[3]));
+  v[0] = cadd(y0, y2);
+  v[2] = csub(y0, y2);
+  v[1] = cadd(y1, y3);
+  v[3] = csub(y1, y3);
+}
+template <bool INV>
+__host__ __device__ __forceinline__ void dft8(double2* v) {
+  constexpr double c = 0.70710678118654752440;
+  double2 e[4] = {v[0], v[2], v[4], v[6]};
+  double2 o[4] = {v[1], v[3], v[5], v[7]};
+  dft4<INV>(e);
+  dft4<INV>(o);
+  // o[k] *= w8^k (forward w8 = e^{-i pi/4}; inverse conjugate)
+  const double2 o1 = INV ? make_double2(c * (o[1].x - o[1].y), c * (o[1].x + o[1].y))
+                         : make_double2(c * (o[1].x + o[1].y), c * (o[1].y - o[1].x));
+  const double2 o2 = mul_mi<INV>(o[2]);
+  const double2 o3 = INV ? make_double2(-c * (o[3].x + o[3].y), c * (o[3].x - o[3].y))
+                         : make_double2(c * (o[3].y - o[3].x), -c * (o[3].x + o[3].y));
+  v[0] = cadd(e[0], o[0]);
+  v[4] = csub(e[0], o[0]);
+  v[1] = cadd(e[1], o1);
+  v[5] = csub(e[1], o1);
+  v[2] = cadd(e[2], o2);
+  v[6] = csub(e[2], o2);
+  v[3] = cadd(e[3], o3);
+  v[7] = csub(e[3], o3);
+}
+template <int R, bool INV>
+__host__ __device__ __forceinline__ void dftR(double2* v) {
+  if constexpr (R == 8) dft8<INV>(v);
+  else if constexpr (R == 4) dft4<INV>(v);
+  else dft2<INV>(v);
+}
+
+template <int N, int PASS>
+struct FftPass {
+  static constexpr int L = ilog2_c(N);
+  static constexpr int n8 = L / 3;
+  static constexpr int rem = L % 3;
+  static constexpr int NP = n8 + (rem ? 1 : 0);
+  static constexpr int R = PASS < n8 ? 8 : (rem == 2 ? 4 : 2);
+  static constexpr int NS = 1 << (3 * PASS);
+  static constexpr bool LAST = PASS == NP - 1;
+};
+
+// One Stockham pass for team thread t: 8/R butterflies b = t + (N/8) q.
+// Input index of (q, r): b + r N/R; output index: (b - k) R + k + r NS.
+template <int N, int PASS, bool INV>
+__host__ __device__ __forceinline__ void fft_pass_compute(double2* v, int t, const double2* __restrict__ tw) {
+  using P = FftPass<N, PASS>;
+  constexpr int R = P::R, G = 8 / R, T = N / 8;
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const int b = t + T * q;
+    const int k = b & (P::NS - 1);
+    if (P::NS > 1) {
+      constexpr int S = N / (P::NS * R);
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+#ifdef __CUDA_ARCH__
+        v[q * R + r] = cmul_tw<INV>(v[q * R + r], __ldg(tw + r * k * S));
+#else
+        v[q * R + r] = cmul_tw<INV>(v[q * R + r], tw[r * k * S]);
+#endif
+      }
+    }
+    dftR<R, INV>(v + q * R);
+  }
+}
+template <int N, int PASS>
+__host__ __device__ __forceinline__ int fft_in_index(int t, int q, int r) {
+  using P = FftPass<N, PASS>;
+  return t + (N / 8) * q + r * (N / P::R);
+}
+template <int N, int PASS>
+__host__ __device__ __forceinline__ int fft_out_index(int t, int q, int r) {
+  using P = FftPass<N, PASS>;
+  const int b = t + (N / 8) * q;
+  const int k = b & (P::NS - 1);
+  return (b - k) * P::R + k + r * P::NS;
+}
+
+#ifdef __CUDACC__
+// All threads of the CTA must call this (it synchronises with __syncthreads).
+// buf: this team's padded buffer (FftSize<N>::kPadded double2). load(i) gives
+// input element i; store(i, v) receives output element i (natural order).
+// Threads with active == false only take part in the barriers. The caller
+// must __syncthreads() before reusing buf or reading what store() wrote to
+// shared memory.
+template <int N, bool INV, int PASS = 0, class Load, class Store>
+__device__ __forceinline__ void fft_team(double2* buf, const double2* __restrict__ tw, int t, bool active, Load& load,
+                                         Store& store) {
+  using P = FftPass<N, PASS>;
+  constexpr int R = P::R, G = 8 / R;
+  double2 v[8];
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = fft_in_index<N, PASS>(t, q, r);
+        if constexpr (PASS == 0) v[q * R + r] = load(i);
+        else v[q * R + r] = buf[fpad(i)];
+      }
+    fft_pass_compute<N, PASS, INV>(v, t, tw);
+  }
+  if constexpr (P::LAST) {
+    __syncthreads();  // store() may target buf: all reads of this pass come first
+    if (active) {
+#pragma unroll
+      for (int q = 0; q < G; ++q)
+#pragma unroll
+        for (int r = 0; r < R; ++r) store(fft_out_index<N, PASS>(t, q, r), v[q * R + r]);
+    }
+  } else {
+    __syncthreads();  // every read of buf in this pass precedes the in-place writes
+    if (active) {
+#pragma unroll
+      for (int q = 0; q < G; ++q)
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[fpad(fft_out_index<N, PASS>(t, q, r))] = v[q * R + r];
+    }
+    __syncthreads();
+    fft_team<N, INV, PASS + 1>(buf, tw, t, active, load, store);
+  }
+}
+#endif
 
 // Device twiddle table exp(-2 pi i m / N), m in [0, N); cached per length.
 const double2* twiddle_table(int n);
