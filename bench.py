@@ -161,7 +161,7 @@ def group_size(dim, requested):
     """Mirror of Problem::group(): vectors per L2-resident BVE sweep group."""
     if requested > 0:
         return requested
-    return max(1, int(80e6 / (6.0 * 8.0 * dim)))
+    return max(1, int(4e9 / (6.0 * 8.0 * dim)))
 
 
 def algorithmic_bytes_per_hvp(n_grid_points, stages, s):

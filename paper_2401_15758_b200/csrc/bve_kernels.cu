@@ -45,7 +45,8 @@ struct Cfg {
   static constexpr size_t kXBytes = kTileBytes > kFftBytes ? kTileBytes : kFftBytes;
   static constexpr size_t kStageSmem = kTileBytes + kXBytes;
   static constexpr size_t kRowSmem = kFftBytes;
-  static constexpr size_t kColSmem = sizeof(double2) * kPad * kCW;
+  static constexpr int kColStride = kPad + 2;  // team buffers 8 banks apart (conflict-free staging)
+  static constexpr size_t kColSmem = sizeof(double2) * kColStride * kCW;
 };
 
 // Packed half spectra (ra, rb) of two real rows -> element i of the full
@@ -91,6 +92,16 @@ __device__ __forceinline__ double arakawa12(const double a[3][3], const double b
 __device__ __forceinline__ double lap5(const double o[3][3]) {
   return o[1][0] + o[1][2] + o[0][1] + o[2][1] - 4.0 * o[1][1];
 }
+// Asynchronous global -> shared 16-byte copy (LDGSTS): every copy of a tile is
+// in flight at once instead of one load-use round trip per element.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void shift3(double w[3][3]) {
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -161,10 +172,11 @@ __global__ void __launch_bounds__(Cfg<N>::kCW*(N / 8)) col_kernel(double2* __res
   double2* base = s + v * N * (N / 2) + kx0;
   for (int e = threadIdx.x; e < C::kCW * N; e += kTh) {
     const int y = e / C::kCW, c = e % C::kCW;
-    sm[c * C::kPad + fpad(y)] = base[static_cast<long long>(y) * (N / 2) + c];
+    cp_async16(sm + c * C::kColStride + fpad(y), base + static_cast<long long>(y) * (N / 2) + c);
   }
+  cp_async_wait_all();
   __syncthreads();
-  double2* buf = sm + team * C::kPad;
+  double2* buf = sm + team * C::kColStride;
   auto ld_own = [&](int i) { return buf[fpad(i)]; };
   auto st_own = [&](int i, double2 z) { buf[fpad(i)] = z; };
   fft_team<N, false>(buf, tw, t, true, ld_own, st_own);
@@ -187,13 +199,13 @@ __global__ void __launch_bounds__(Cfg<N>::kCW*(N / 8)) col_kernel(double2* __res
   __syncthreads();
   for (int e = threadIdx.x; e < C::kCW * N; e += kTh) {
     const int y = e / C::kCW, c = e % C::kCW;
-    base[static_cast<long long>(y) * (N / 2) + c] = sm[c * C::kPad + fpad(y)];
+    base[static_cast<long long>(y) * (N / 2) + c] = sm[c * C::kColStride + fpad(y)];
   }
 }
 
 // --------------------------------------------------------- fused RK stage --
 template <int N, int MODE>
-__global__ void __launch_bounds__(kThreads) stage_kernel(StageArgs p) {
+__global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
   using C = Cfg<N>;
   constexpr int T = C::kT, R = T + 2;
   extern __shared__ double smd[];
@@ -235,50 +247,69 @@ __global__ void __launch_bounds__(kThreads) stage_kernel(StageArgs p) {
   // Phase 2: stencil-input rows (overwrite the FFT buffers).
   if (MODE != kModeAdj) {
     const double* xin = p.x_in + off;
-    for (int e = tid; e < R * N; e += kThreads) {
+    for (int e = 2 * tid; e < R * N; e += 2 * kThreads) {
       const int r = e / N, x = e % N;
-      X[e] = xin[static_cast<long long>((y0 - 1 + r) & (N - 1)) * N + x];
+      cp_async16(X + e, xin + static_cast<long long>((y0 - 1 + r) & (N - 1)) * N + x);
     }
+    cp_async_wait_all();
   } else {
+    // lambda/mu combination of SURVEY.md B.1, batched kB elements per thread
+    // (all loads issued before any dependent arithmetic).
     const double dt = p.dt;
-    for (int e = tid; e < R * N; e += kThreads) {
-      const int r = e / N, x = e % N;
-      const int gy = (y0 - 1 + r) & (N - 1);
-      const long long g = off + static_cast<long long>(gy) * N + x;
-      const bool owned = r >= 1 && r <= T;
-      const double mu = has_prev ? p.q_in[g] + P[e] : 0.0;
-      if (finish) {
-        if (owned) p.d[g] = p.acc[g] + mu;
-        continue;
+    const double* __restrict__ qin = p.q_in;
+    double* __restrict__ lamp = p.d;
+    double* __restrict__ accp = p.acc;
+    constexpr int kB = 4;
+#pragma unroll 1
+    for (int e0 = tid; e0 < R * N; e0 += kB * kThreads) {
+      double qv[kB], av[kB], lv[kB];
+      long long gg[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int e = min(e0 + u * kThreads, R * N - 1);  // tail lanes redo the last element
+        const int r = e / N, x = e % N;
+        gg[u] = off + static_cast<long long>((y0 - 1 + r) & (N - 1)) * N + x;
+        qv[u] = has_prev ? qin[gg[u]] : 0.0;
+        av[u] = (finish || p.stage <= 1 || (p.stage == 3 && has_prev)) ? accp[gg[u]] : 0.0;
+        lv[u] = (finish || (p.stage == 3 && has_prev)) ? 0.0 : lamp[gg[u]];
       }
-      double a;
-      switch (p.stage) {
-        case 3: {
-          const double lam = has_prev ? p.acc[g] + mu : p.d[g];
-          if (owned && has_prev) p.d[g] = lam;
-          a = dt / 6.0 * lam;
-          break;
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int e = e0 + u * kThreads;
+        if (e >= R * N) break;
+        const int r = e / N;
+        const bool owned = r >= 1 && r <= T;
+        const double mu = has_prev ? qv[u] + P[e] : 0.0;
+        if (finish) {
+          if (owned) lamp[gg[u]] = av[u] + mu;
+          continue;
         }
-        case 2: {
-          const double lam = p.d[g];
-          if (owned) p.acc[g] = lam + mu;
-          a = dt / 3.0 * lam + dt * mu;
-          break;
+        double a;
+        switch (p.stage) {
+          case 3: {
+            const double lam = has_prev ? av[u] + mu : lv[u];
+            if (owned && has_prev) lamp[gg[u]] = lam;
+            a = dt / 6.0 * lam;
+            break;
+          }
+          case 2: {
+            if (owned) accp[gg[u]] = lv[u] + mu;
+            a = dt / 3.0 * lv[u] + dt * mu;
+            break;
+          }
+          case 1: {
+            if (owned) accp[gg[u]] = av[u] + mu;
+            a = dt / 3.0 * lv[u] + 0.5 * dt * mu;
+            break;
+          }
+          default: {
+            if (owned) accp[gg[u]] = av[u] + mu;
+            a = dt / 6.0 * lv[u] + 0.5 * dt * mu;
+            break;
+          }
         }
-        case 1: {
-          const double lam = p.d[g];
-          if (owned) p.acc[g] += mu;
-          a = dt / 3.0 * lam + 0.5 * dt * mu;
-          break;
-        }
-        default: {
-          const double lam = p.d[g];
-          if (owned) p.acc[g] += mu;
-          a = dt / 6.0 * lam + 0.5 * dt * mu;
-          break;
-        }
+        X[e] = a;
       }
-      X[e] = a;
     }
     if (finish) return;
   }

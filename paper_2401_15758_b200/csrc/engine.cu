@@ -139,10 +139,12 @@ Problem::Problem(const ProblemDesc& d, long long n_obs, const long long* idx, co
 int Problem::group() const {
   if (d_.model != kModelBVE) return 1 << 30;
   if (d_.block_group > 0) return d_.block_group;
-  // Keep a group's sweep working set (D, A, X0, X1, S0, S1 ~ 6 fields per
-  // vector) within ~80 MB of the 126 MB L2.
+  // Whole block per launch (measured on B200: per-vector stage time is flat
+  // or falls with the group size, and L2 residency of small groups did not
+  // pay — the stage kernels are issue/latency bound, not bandwidth bound),
+  // capped so the sweep workspace (~6 fields per vector) stays under ~4 GB.
   const double per = 6.0 * 8.0 * static_cast<double>(dim_);
-  return std::max(1, static_cast<int>(80e6 / per));
+  return std::max(1, static_cast<int>(4e9 / per));
 }
 
 void Problem::ensure_work(int nvec) const {
