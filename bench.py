@@ -170,7 +170,7 @@ def algorithmic_bytes_per_hvp(n_grid_points, stages, s):
 
 
 # --------------------------------------------------------- CPU baseline -----
-def cpu_reference_sample(cfg, budget_s=20.0):
+def cpu_reference_sample(cfg, budget_s=10.0):
     """Oracle port of the reference path on all host threads; bounded sample.
 
     Each thread owns one vector and runs TLM then ADJ over a short window of the
@@ -187,20 +187,26 @@ def cpu_reference_sample(cfg, budget_s=20.0):
 
     spec = scenario.CONFIGS[cfg]
     cores = os.cpu_count() or 1
-    # sample window: a few steps, sized so one vector-thread takes ~budget/2
-    k = {0: spec.steps, 1: 100, 2: 20, 3: 2, 4: 4}[cfg]
-    osc = O.Scenario(cfg, steps=k, spi=k)
-    tr = osc.linearize(osc.background)
-    V = O.gaussian_matrix(osc.n, cores, 5)
+    V = O.gaussian_matrix(spec.dim, cores, 5)
 
-    def one(j):
-        y = tr.tlm_range(0, k, V[j])
-        return tr.adj_range(0, k, y)
+    def timed(k):
+        osc = O.Scenario(cfg, steps=k, spi=k)
+        tr = osc.linearize(osc.background)
 
-    t0 = time.perf_counter()
-    with cf.ThreadPoolExecutor(cores) as ex:
-        list(ex.map(one, range(cores)))
-    dt = time.perf_counter() - t0
+        def one(j):
+            y = tr.tlm_range(0, k, V[j])
+            return tr.adj_range(0, k, y)
+
+        t0 = time.perf_counter()
+        with cf.ThreadPoolExecutor(cores) as ex:
+            list(ex.map(one, range(cores)))
+        return time.perf_counter() - t0
+
+    # calibrate the window so the timed sample is ~budget_s of wall time
+    k = 1
+    dt = timed(k)
+    k = max(1, min(spec.steps, int(round(k * budget_s / max(dt, 1e-3)))))
+    dt = timed(k)
     hvp_equiv = cores * k / spec.steps
     return {"value": hvp_equiv / dt, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": (f"{cores} vectors x (TLM+ADJ over {k} of {spec.steps} RK4 steps) on the {spec.name} grid, "
