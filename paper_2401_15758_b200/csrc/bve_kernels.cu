@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
   const bool finish = MODE == kModeAdj && (p.flags & kFlagFinish);
 
   // Phase 1: inverse x-FFT of rows y0-1 .. y0+T -> P.
-  if (has_prev) {
+  if (has_prev && !(p.flags & kFlagSkipInvFft)) {
     constexpr int kPairs = R / 2;
 #pragma unroll 1
     for (int b0 = 0; b0 < kPairs; b0 += C::kTeams) {
@@ -321,94 +321,209 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
   const double js = p.inv12h2, ls = p.invh2, nu = p.nu, dt = p.dt;
   const int xt = tid % C::kNCT, rg = tid / C::kNCT;
   const int r0 = 1 + rg * C::kRPG;  // first owned smem row of this group
-  double res[C::kCPT][C::kRPG];
+  double res[C::kCPT][C::kRPG] = {};
+  // Two sweeps per column strip, each with one shared-memory window (X or P)
+  // and one global base-field window whose next row is prefetched one step
+  // ahead (halves the live windows, keeps global loads in flight):
+  //   TLM  A: J(psi_b, X) + nu Lap X        B: + J(P, omega_b), RK4 update
+  //   ADJ  A: q = -J(psi_b, a) + nu Lap a   B: r = -J(a, omega_b)
+  //   NL   one smem-only sweep: J(P, X) + nu Lap X, RK4 update
+  auto sweep = [&](int cc, const double* S, const double* G, auto pass_c, double(&rc)[C::kRPG]) {
+    constexpr int pass = decltype(pass_c)::value;
+    {
+      const int x = xt + cc * C::kNCT;
+      const int xs[3] = {(x - 1) & (N - 1), x, (x + 1) & (N - 1)};
+      auto grow = [&](int r, double* w) {
+        const double* row = G + static_cast<long long>((y0 + r - 1) & (N - 1)) * N;
 #pragma unroll
-  for (int cc = 0; cc < C::kCPT; ++cc) {
-    const int x = xt + cc * C::kNCT;
-    const int xs[3] = {(x - 1) & (N - 1), x, (x + 1) & (N - 1)};
-    double wx[3][3], wp[3][3], bp[3][3], bw[3][3];
-    auto gload = [&](const double* f, int r, double* w) {
-      const double* row = f + static_cast<long long>((y0 + r - 1) & (N - 1)) * N;
+        for (int c = 0; c < 3; ++c) w[c] = __ldg(row + xs[c]);
+      };
+      double ws[3][3], wg[3][3], gn[3];
+      double dn = 0.0, an = 0.0;  // prefetched RK state (TLM pass B)
+      const bool rk = MODE == kModeTlm && pass == 1;
+      auto rkload = [&](int r) {
+        const long long g = off + static_cast<long long>((y0 + r - 1) & (N - 1)) * N + x;
+        if (p.stage <= 2) dn = p.d[g];
+        if (p.stage >= 1) an = p.acc[g];
+      };
 #pragma unroll
-      for (int c = 0; c < 3; ++c) w[c] = __ldg(row + xs[c]);
-    };
+      for (int dy = 0; dy < 2; ++dy) {
 #pragma unroll
-    for (int dy = 0; dy < 2; ++dy) {
-      const int r = r0 - 1 + dy;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        wx[dy][c] = X[r * N + xs[c]];
-        if (MODE != kModeAdj) wp[dy][c] = P[r * N + xs[c]];
+        for (int c = 0; c < 3; ++c) ws[dy][c] = S[(r0 - 1 + dy) * N + xs[c]];
+        grow(r0 - 1 + dy, wg[dy]);
       }
-      if (MODE != kModeNl) {
-        gload(p.base_p, r, bp[dy]);
-        gload(p.base_w, r, bw[dy]);
+      grow(r0 + 1, gn);
+      if (rk) rkload(r0);
+#pragma unroll
+      for (int q = 0; q < C::kRPG; ++q) {
+        const int r = r0 + q;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          ws[2][c] = S[(r + 1) * N + xs[c]];
+          wg[2][c] = gn[c];
+        }
+        if (q + 1 < C::kRPG) grow(r + 2, gn);
+        const double dcur = dn, acur = an;
+        if (rk && q + 1 < C::kRPG) rkload(r + 1);
+        const long long g = off + static_cast<long long>((y0 + r - 1) & (N - 1)) * N + x;
+        if (MODE == kModeTlm) {
+          if (pass == 0) {
+            rc[q] = arakawa12(wg, ws) * js + nu * lap5(ws) * ls;
+          } else {
+            const double kk = rc[q] + arakawa12(ws, wg) * js;
+            double out;
+            switch (p.stage) {
+              case 0:
+                p.acc[g] = dcur + dt / 6.0 * kk;
+                out = dcur + 0.5 * dt * kk;
+                p.x_out[g] = out;
+                break;
+              case 1:
+                p.acc[g] = acur + dt / 3.0 * kk;
+                out = dcur + 0.5 * dt * kk;
+                p.x_out[g] = out;
+                break;
+              case 2:
+                p.acc[g] = acur + dt / 3.0 * kk;
+                out = dcur + dt * kk;
+                p.x_out[g] = out;
+                break;
+              default:
+                out = acur + dt / 6.0 * kk;
+                p.d[g] = out;
+                break;
+            }
+            rc[q] = out;
+          }
+        } else {  // ADJ
+          if (pass == 0) p.q_out[g] = -arakawa12(wg, ws) * js + nu * lap5(ws) * ls;
+          else rc[q] = -arakawa12(ws, wg) * js;
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          ws[0][c] = ws[1][c];
+          ws[1][c] = ws[2][c];
+          wg[0][c] = wg[1][c];
+          wg[1][c] = wg[2][c];
+        }
       }
     }
+  };
+  if (!(p.flags & kFlagSkipStencil)) {
+    if (MODE == kModeTlm) {
 #pragma unroll
-    for (int q = 0; q < C::kRPG; ++q) {
-      const int r = r0 + q;
+      for (int cc = 0; cc < C::kCPT; ++cc) {
+        double rc[C::kRPG];
+        sweep(cc, X, p.base_p, std::integral_constant<int, 0>{}, rc);
+        sweep(cc, P, p.base_w, std::integral_constant<int, 1>{}, rc);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        wx[2][c] = X[(r + 1) * N + xs[c]];
-        if (MODE != kModeAdj) wp[2][c] = P[(r + 1) * N + xs[c]];
+        for (int q = 0; q < C::kRPG; ++q) res[cc][q] = rc[q];
       }
-      if (MODE != kModeNl) {
-        gload(p.base_p, r + 1, bp[2]);
-        gload(p.base_w, r + 1, bw[2]);
-      }
-      const int gy = (y0 + r - 1) & (N - 1);
-      const long long g = off + static_cast<long long>(gy) * N + x;
-      double out;
-      if (MODE == kModeNl) {
-        out = arakawa12(wp, wx) * js + nu * lap5(wx) * ls;
-        if (p.store_w) {
-          p.store_w[static_cast<long long>(gy) * N + x] = wx[1][1];
-          p.store_p[static_cast<long long>(gy) * N + x] = wp[1][1];
+    } else if (MODE == kModeAdj) {
+      // one sweep, one smem window (a) and two prefetched base windows
+#pragma unroll 1
+      for (int cc = 0; cc < C::kCPT; ++cc) {
+        const int x = xt + cc * C::kNCT;
+        const int xs[3] = {(x - 1) & (N - 1), x, (x + 1) & (N - 1)};
+        auto grow = [&](const double* G, int r, double* w) {
+          const double* row = G + static_cast<long long>((y0 + r - 1) & (N - 1)) * N;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) w[c] = __ldg(row + xs[c]);
+        };
+        double wa[3][3], bp[3][3], bw[3][3], pn[3], wn[3];
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) wa[dy][c] = X[(r0 - 1 + dy) * N + xs[c]];
+          grow(p.base_p, r0 - 1 + dy, bp[dy]);
+          grow(p.base_w, r0 - 1 + dy, bw[dy]);
         }
-      } else if (MODE == kModeTlm) {
-        out = (arakawa12(bp, wx) + arakawa12(wp, bw)) * js + nu * lap5(wx) * ls;
-      } else {
-        p.q_out[g] = -arakawa12(bp, wx) * js + nu * lap5(wx) * ls;
-        out = -arakawa12(wx, bw) * js;
-      }
-      if (MODE != kModeAdj) {
-        const double kk = out;
-        switch (p.stage) {
-          case 0: {
-            const double d = p.d[g];
-            p.acc[g] = d + dt / 6.0 * kk;
-            out = d + 0.5 * dt * kk;
-            p.x_out[g] = out;
-            break;
+        grow(p.base_p, r0 + 1, pn);
+        grow(p.base_w, r0 + 1, wn);
+#pragma unroll
+        for (int q = 0; q < C::kRPG; ++q) {
+          const int r = r0 + q;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            wa[2][c] = X[(r + 1) * N + xs[c]];
+            bp[2][c] = pn[c];
+            bw[2][c] = wn[c];
           }
-          case 1: {
-            const double d = p.d[g];
-            p.acc[g] += dt / 3.0 * kk;
-            out = d + 0.5 * dt * kk;
-            p.x_out[g] = out;
-            break;
+          if (q + 1 < C::kRPG) {
+            grow(p.base_p, r + 2, pn);
+            grow(p.base_w, r + 2, wn);
           }
-          case 2: {
-            const double d = p.d[g];
-            p.acc[g] += dt / 3.0 * kk;
-            out = d + dt * kk;
-            p.x_out[g] = out;
-            break;
-          }
-          default: {
-            out = p.acc[g] + dt / 6.0 * kk;
-            p.d[g] = out;
-            break;
-          }
+          const long long g = off + static_cast<long long>((y0 + r - 1) & (N - 1)) * N + x;
+          p.q_out[g] = -arakawa12(bp, wa) * js + nu * lap5(wa) * ls;
+          const double out = -arakawa12(wa, bw) * js;
+          if (cc == 0) res[0][q] = out;
+          else res[C::kCPT - 1][q] = out;
+          shift3(wa);
+          shift3(bp);
+          shift3(bw);
         }
       }
-      res[cc][q] = out;
-      shift3(wx);
-      if (MODE != kModeAdj) shift3(wp);
-      if (MODE != kModeNl) {
-        shift3(bp);
-        shift3(bw);
+    } else {
+#pragma unroll
+      for (int cc = 0; cc < C::kCPT; ++cc) {
+        const int x = xt + cc * C::kNCT;
+        const int xs[3] = {(x - 1) & (N - 1), x, (x + 1) & (N - 1)};
+        double wx[3][3], wp[3][3];
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            wx[dy][c] = X[(r0 - 1 + dy) * N + xs[c]];
+            wp[dy][c] = P[(r0 - 1 + dy) * N + xs[c]];
+          }
+#pragma unroll
+        for (int q = 0; q < C::kRPG; ++q) {
+          const int r = r0 + q;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            wx[2][c] = X[(r + 1) * N + xs[c]];
+            wp[2][c] = P[(r + 1) * N + xs[c]];
+          }
+          const int gy = (y0 + r - 1) & (N - 1);
+          const long long g = off + static_cast<long long>(gy) * N + x;
+          if (p.store_w) {
+            p.store_w[static_cast<long long>(gy) * N + x] = wx[1][1];
+            p.store_p[static_cast<long long>(gy) * N + x] = wp[1][1];
+          }
+          const double kk = arakawa12(wp, wx) * js + nu * lap5(wx) * ls;
+          double out;
+          switch (p.stage) {
+            case 0: {
+              const double d = p.d[g];
+              p.acc[g] = d + dt / 6.0 * kk;
+              out = d + 0.5 * dt * kk;
+              p.x_out[g] = out;
+              break;
+            }
+            case 1: {
+              const double d = p.d[g];
+              p.acc[g] += dt / 3.0 * kk;
+              out = d + 0.5 * dt * kk;
+              p.x_out[g] = out;
+              break;
+            }
+            case 2: {
+              const double d = p.d[g];
+              p.acc[g] += dt / 3.0 * kk;
+              out = d + dt * kk;
+              p.x_out[g] = out;
+              break;
+            }
+            default: {
+              out = p.acc[g] + dt / 6.0 * kk;
+              p.d[g] = out;
+              break;
+            }
+          }
+          res[cc][q] = out;
+          shift3(wx);
+          shift3(wp);
+        }
       }
     }
   }
@@ -422,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
   // Phase 4: forward x-FFT of the owned rows -> next row spectra.
   constexpr int kOwnPairs = T / 2;
 #pragma unroll 1
-  for (int b0 = 0; b0 < kOwnPairs; b0 += C::kTeams) {
+  for (int b0 = 0; b0 < ((p.flags & kFlagSkipFwdFft) ? 0 : kOwnPairs); b0 += C::kTeams) {
     const int pr = b0 + team;
     const bool act = pr < kOwnPairs;
     const double* pa = P + (1 + 2 * pr) * N;

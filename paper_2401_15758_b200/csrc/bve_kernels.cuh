@@ -6,7 +6,14 @@
 namespace sdv {
 
 enum StageMode { kModeTlm = 0, kModeAdj = 1, kModeNl = 2 };
-enum StageFlags { kFlagHasPrev = 1, kFlagFinish = 2 };
+enum StageFlags {
+  kFlagHasPrev = 1,
+  kFlagFinish = 2,
+  // timing experiments only (probe): skip a phase, results are garbage
+  kFlagSkipInvFft = 16,
+  kFlagSkipStencil = 32,
+  kFlagSkipFwdFft = 64
+};
 
 // Arguments of one fused RK stage launch over a group of vectors.
 //   TLM/NL: d = step-start state, acc = RK accumulator, x_in = stage input

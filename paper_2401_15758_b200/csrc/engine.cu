@@ -12,6 +12,7 @@
 //   Problem::prior_sqrt     <- PriorCovariance::apply_sqrt (src/prior.cpp:64-69), Fourier-diagonal B
 #include <cmath>
 #include <map>
+#include <cstdlib>
 #include <mutex>
 
 #include "engine.hpp"
@@ -456,6 +457,8 @@ void Problem::probe_stage_kernels(const Trajectory& tr, int s, int stages, float
       SDV_CUDA(cudaEventRecord(ev[1], st_));
       StageArgs a = bve_args(d_);
       a.stage = sg;
+      // SDV_PROBE_FLAGS (timing experiments): skip phases, see kFlagSkip*.
+      if (const char* e = std::getenv("SDV_PROBE_FLAGS")) a.flags = std::atoi(e);
       a.s_in = s_cur;
       a.s_out = s_nxt;
       a.x_in = sg == 0 ? dst : xb[(sg - 1) & 1];
