@@ -164,22 +164,19 @@ __global__ void __launch_bounds__(Cfg<N>::kCW*(N / 8)) col_kernel(double2* __res
                                                                   const double* __restrict__ sym,
                                                                   const double2* __restrict__ tw) {
   using C = Cfg<N>;
-  constexpr int kTh = C::kCW * C::kTeam;
   extern __shared__ double2 sm[];
-  const int team = threadIdx.x / C::kTeam, t = threadIdx.x % C::kTeam;
+  // Lanes interleave the kCW columns (team = column), so every warp-wide
+  // global access covers kCW adjacent double2 of a few rows (coalesced); the
+  // first forward pass reads global memory directly and the last inverse
+  // pass writes it back (no staging pass).
+  const int team = threadIdx.x % C::kCW, t = threadIdx.x / C::kCW;
   const int kx0 = blockIdx.x * C::kCW;
   const long long v = blockIdx.y;
-  double2* base = s + v * N * (N / 2) + kx0;
-  for (int e = threadIdx.x; e < C::kCW * N; e += kTh) {
-    const int y = e / C::kCW, c = e % C::kCW;
-    cp_async16(sm + c * C::kColStride + fpad(y), base + static_cast<long long>(y) * (N / 2) + c);
-  }
-  cp_async_wait_all();
-  __syncthreads();
+  double2* col = s + v * N * (N / 2) + kx0 + team;
   double2* buf = sm + team * C::kColStride;
-  auto ld_own = [&](int i) { return buf[fpad(i)]; };
+  auto ld_glob = [&](int i) { return col[static_cast<long long>(i) * (N / 2)]; };
   auto st_own = [&](int i, double2 z) { buf[fpad(i)] = z; };
-  fft_team<N, false>(buf, tw, t, true, ld_own, st_own);
+  fft_team<N, false>(buf, tw, t, true, ld_glob, st_own);
   __syncthreads();
   const int kx = kx0 + team;
   const double* sk = sym + static_cast<long long>(kx) * N;
@@ -195,12 +192,8 @@ __global__ void __launch_bounds__(Cfg<N>::kCW*(N / 8)) col_kernel(double2* __res
     const double2 zm = buf[fpad((N - ky) & (N - 1))];
     return make_double2(pp * z.x + mm * zm.x, pp * z.y - mm * zm.y);
   };
-  fft_team<N, true>(buf, tw, t, true, ld_mul, st_own);
-  __syncthreads();
-  for (int e = threadIdx.x; e < C::kCW * N; e += kTh) {
-    const int y = e / C::kCW, c = e % C::kCW;
-    base[static_cast<long long>(y) * (N / 2) + c] = sm[c * C::kColStride + fpad(y)];
-  }
+  auto st_glob = [&](int i, double2 z) { col[static_cast<long long>(i) * (N / 2)] = z; };
+  fft_team<N, true>(buf, tw, t, true, ld_mul, st_glob);
 }
 
 // --------------------------------------------------------- fused RK stage --

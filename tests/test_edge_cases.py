@@ -1,0 +1,116 @@
+"""Edge cases of the boundary and the CUDA path, after the reference's own
+tests: validation errors (proj/src/fourdvar.cpp:25-58), homogeneity
+(proj/tests/test_burgers.cpp:122-129), determinism
+(proj/tests/test_sketching.cpp:474-490), non-finite detection
+(proj/tests/test_burgers.cpp:174-178), worker/group independence
+(proj/tests/test_sketching.cpp:463-472)."""
+import numpy as np
+import pytest
+
+
+def _args(model=1, n=64, n_t=2, spi=3, idx=(0, 4, 8), var=1e-4):
+    idx = np.asarray(idx, np.int64)
+    vals = np.zeros((n_t, idx.size))
+    variances = np.full((n_t, idx.size), var)
+    dim = n if model == 1 else n * n
+    return (model, n, 1e-3, 1e-4, n_t, spi, 0.1, 0.05, idx, vals, variances, np.zeros(dim))
+
+
+@pytest.mark.parametrize("bad,msg", [
+    (dict(model=7), "unknown model"),
+    (dict(n=100), "power of two"),
+    (dict(idx=(0, 4, 4)), "strictly increasing"),
+    (dict(idx=(0, 70)), "strictly increasing"),
+    (dict(var=0.0), "variances must be positive"),
+    (dict(n_t=0), "n_t >= 1"),
+])
+def test_problem_validation_raises_invalid_argument(bad, msg):
+    """No GPU needed: validation precedes any CUDA call (SDV_EINVAL -> ValueError)."""
+    from paper_2401_15758_b200 import api
+
+    with pytest.raises(ValueError, match=msg):
+        api.Problem(*_args(**bad))
+
+
+@pytest.mark.gpu
+def test_tlm_exactly_homogeneous_in_powers_of_two(oracle, sdv):
+    from paper_2401_15758_b200 import scenario
+
+    for cfg, steps in [(0, 20), (2, 8)]:
+        osc = oracle.Scenario(cfg, steps=steps, spi=4 if cfg == 2 else -1)
+        prob = scenario.from_arrays(scenario.CONFIGS[cfg], osc.indices, osc.values, osc.variances, osc.background,
+                                    steps=steps, spi=4 if cfg == 2 else None)
+        tr = prob.linearize(osc.background)
+        dx = oracle.gaussian_matrix(osc.n, 1, 42)
+        once = tr.tlm_range(0, steps, dx)
+        twice = tr.tlm_range(0, steps, 2.0 * dx)
+        assert np.array_equal(twice, 2.0 * once)
+        assert not tr.tlm_range(0, steps, np.zeros_like(dx)).any()
+        assert not tr.adj_range(0, steps, np.zeros_like(dx)).any()
+
+
+@pytest.mark.gpu
+def test_results_independent_of_group_size_and_bitwise_deterministic(oracle, sdv):
+    from paper_2401_15758_b200 import scenario
+
+    osc = oracle.Scenario(2, steps=8, spi=4)
+    V = oracle.gaussian_matrix(osc.n, 7, 3)
+    outs = []
+    for g in (0, 1, 3, 7):
+        prob = scenario.from_arrays(scenario.CONFIGS[2], osc.indices, osc.values, osc.variances, osc.background,
+                                    block_group=g, steps=8, spi=4)
+        outs.append(prob.linearize(osc.background).gram(V))
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    prob = scenario.from_arrays(scenario.CONFIGS[2], osc.indices, osc.values, osc.variances, osc.background,
+                                steps=8, spi=4)
+    tr = prob.linearize(osc.background)
+    e1 = tr.sketch(1, 20, 77)[0]
+    e2 = tr.sketch(1, 20, 77)[0]
+    assert np.array_equal(e1, e2)
+
+
+@pytest.mark.gpu
+def test_block_of_one_and_ragged_blocks(oracle, sdv):
+    from paper_2401_15758_b200 import scenario
+
+    osc = oracle.Scenario(2, steps=8, spi=4)
+    prob = scenario.from_arrays(scenario.CONFIGS[2], osc.indices, osc.values, osc.variances, osc.background,
+                                block_group=4, steps=8, spi=4)
+    tr = prob.linearize(osc.background)
+    otr = osc.linearize(osc.background)
+    V = oracle.gaussian_matrix(osc.n, 10, 9)  # 10 = 4 + 4 + 2 (ragged last group)
+    G = tr.gram(V)
+    one = tr.gram(V[3:4])
+    assert np.array_equal(one[0], G[3])
+    for j in (0, 5, 9):
+        ref = otr.gram(V[j:j + 1])[0]
+        assert np.linalg.norm(G[j] - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+@pytest.mark.gpu
+def test_nonfinite_state_raises_runtime_error(sdv):
+    """Over-CFL forward integration must fail loudly (proj/src/bve.cpp:120-124)."""
+    from paper_2401_15758_b200 import api
+
+    n = 64
+    x0 = 1e3 * api.gaussian_vector(n * n, 5)
+    prob = api.Problem(2, n, 1e-4, 5.0, 2, 20, 0.2, 0.3, np.zeros(0, np.int64), np.zeros(0), np.zeros(0), x0)
+    with pytest.raises(sdv.SdvError, match="non-finite"):
+        prob.linearize(x0)
+
+
+@pytest.mark.gpu
+def test_step_range_validation(sdv):
+    from paper_2401_15758_b200 import api
+
+    n = 64
+    prob = api.Problem(1, n, 1e-3, 1e-4, 2, 5, 0.1, 0.05, np.array([0, 8]), np.zeros((2, 2)), np.full((2, 2), 1e-4),
+                       np.zeros(n))
+    tr = prob.linearize(np.sin(np.arange(n)))
+    with pytest.raises(ValueError):
+        tr.tlm_range(5, 2, np.ones(n))
+    with pytest.raises(ValueError):
+        tr.adj_range(0, 11, np.ones(n))
+    with pytest.raises(ValueError):
+        tr.state_at(11)

@@ -152,19 +152,29 @@ def test_pcg_iterations_parity(oracle, sdv):
     assert rel(x_plain, xd) <= 1e-7 and rel(x_pre, xd) <= 1e-7
 
 
-@pytest.mark.parametrize("cfg,mode,method", [(0, 1, 0), (0, 1, 1), (0, 1, 2), (0, 3, 0), (0, 0, 0), (0, 2, 1),
-                                             (1, 1, 0)])
-def test_gn_solve_parity(oracle, sdv, cfg, mode, method):
-    """Final analysis <= 1e-8 relative, PCG counts +-1 per GN step, same counters."""
-    osc, prob = pair(oracle, cfg)
+@pytest.mark.parametrize("cfg,mode,method,steps,iters", [
+    (0, 1, 0, -1, -1), (0, 1, 1, -1, -1), (0, 1, 2, -1, -1), (0, 3, 0, -1, -1), (0, 0, 0, -1, -1),
+    (0, 2, 1, -1, -1), (0, 2, 0, -1, -1), (0, 2, 2, -1, -1), (0, 4, 0, -1, -1), (0, 5, 0, -1, -1),
+    (1, 1, 0, -1, -1), (2, 2, 1, 20, 2)])
+def test_gn_solve_parity(oracle, sdv, cfg, mode, method, steps, iters):
+    """Final analysis <= 1e-8 relative, PCG counts +-1 per GN step, same counters.
+
+    Modes: 0 SketchSolv, 1 SketchPrec, 2 SketchPrecA (adaptive + reuse),
+    3 PrecGamma, 4 PrecLanczos, 5 PrecALanczos; methods 0 RandSVD, 1 Nystrom,
+    2 SingleView."""
+    osc, prob = pair(oracle, cfg, steps=steps)
     from paper_2401_15758_b200 import scenario
 
     kw = scenario.CONFIGS[cfg].gn_kwargs()
     kw.update(mode=mode, method=method)
-    if mode == 2:
+    if mode in (2, 5):
         kw.update(rank=10, growth=10, max_rank=30, rank2=61)
+    if mode in (4, 5):
+        kw.update(rank=12)
+    if iters > 0:
+        kw.update(max_gn_iters=iters)
     ro = osc.gn_solve(mode=mode, method=method, rank=kw["rank"], rank2=kw.get("rank2", -1), growth=kw["growth"],
-                      max_rank=kw["max_rank"], workers=8)
+                      max_rank=kw["max_rank"], max_gn_iters=kw["max_gn_iters"], workers=8)
     rg = prob.gn_solve(**kw)
     assert len(rg["log"]) == len(ro["log"])
     # +-1 PCG iterations per GN step for the sketch-preconditioned modes. The
