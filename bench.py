@@ -45,7 +45,30 @@ def parse():
     ap.add_argument("--sweep", default="", help="extra block widths to report, e.g. 1,8,32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gn", default="", help="also time full GN solves for these configs, e.g. 0,1,2,4 (or 'all')")
     return ap.parse_args()
+
+
+def gn_solve_timing(cfg):
+    """Wall time of a full gn_solve (device-resident: FWD/evaluate, sketch, PCG,
+    More-Thuente) on BASELINE config `cfg`, with its counters."""
+    from paper_2401_15758_b200 import scenario
+
+    sc = scenario.build(cfg)
+    sc.problem.synchronize()
+    t0 = time.perf_counter()
+    r = sc.problem.gn_solve(**sc.spec.gn_kwargs())
+    dt = time.perf_counter() - t0
+    log = r["log"]
+    last = log[-1] if len(log) else [0] * 16
+    import numpy as np
+
+    err_a = float(np.linalg.norm(r["analysis"] - sc.truth0) / np.linalg.norm(sc.truth0))
+    err_b = float(np.linalg.norm(sc.problem.background - sc.truth0) / np.linalg.norm(sc.truth0))
+    return {"config": sc.spec.name, "seconds": dt, "gn_iterations": int(len(log)), "total_pcg": int(r["summary"][2]),
+            "counters": {"fwd": int(last[11]), "tlm": int(last[12]), "adj": int(last[13]),
+                         "offline_tlm": int(last[14]), "offline_adj": int(last[15])},
+            "final_cost": float(r["summary"][0]), "rel_error_analysis": err_a, "rel_error_background": err_b}
 
 
 # ------------------------------------------------------------------ dist ----
@@ -368,6 +391,9 @@ def run_ours(args, world, rank, local):
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches}
         if sweep:
             line["block_sweep"] = sweep
+        if args.gn:
+            cfgs = [0, 1, 2, 3, 4] if args.gn == "all" else [int(x) for x in args.gn.split(",") if x]
+            line["gn_solve"] = [gn_solve_timing(c) for c in cfgs]
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

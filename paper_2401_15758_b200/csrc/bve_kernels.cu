@@ -29,17 +29,20 @@ namespace {
 
 constexpr int kThreads = 256;
 
-template <int N>
+// TT: owned rows per stage CTA (8; 2 for small blocks, where 8-row tiles
+// would leave most SMs idle). CWW: columns per col-kernel CTA (0 = default).
+template <int N, int TT = 8, int CWW = 0>
 struct Cfg {
   static constexpr int kTeam = N / 8;                        // threads per FFT
   static constexpr int kTeams = kThreads / kTeam;            // FFTs in flight per CTA
   static constexpr int kPad = FftSize<N>::kPadded;           // double2 per FFT buffer
-  static constexpr int kT = 8;                               // owned rows per stage CTA
+  static constexpr int kT = TT;                              // owned rows per stage CTA
   static constexpr int kNCT = N < kThreads ? N : kThreads;   // column threads
   static constexpr int kRG = kThreads / kNCT;                // row groups
   static constexpr int kRPG = kT / kRG;                      // rows per group
   static constexpr int kCPT = N / kNCT;                      // columns per thread
-  static constexpr int kCW = (N / 2) < (kThreads / kTeam) ? (N / 2) : (kThreads / kTeam);  // col-kernel columns
+  static constexpr int kCWDefault = (N / 2) < (kThreads / kTeam) ? (N / 2) : (kThreads / kTeam);
+  static constexpr int kCW = CWW > 0 ? CWW : kCWDefault;     // col-kernel columns
   static constexpr size_t kFftBytes = sizeof(double2) * kPad * kTeams;
   static constexpr size_t kTileBytes = sizeof(double) * (kT + 2) * N;
   static constexpr size_t kXBytes = kTileBytes > kFftBytes ? kTileBytes : kFftBytes;
@@ -159,11 +162,10 @@ __global__ void __launch_bounds__(kThreads) row_inv_kernel(const double2* __rest
 // Column kx = 0 holds X(0) + i X(n/2) per row; both are real-input columns, so
 // the multiplier is applied through the Hermitian split
 //   Z'(ky) = (s0+sN)/2 Z(ky) + (s0-sN)/2 conj(Z(-ky)).
-template <int N>
-__global__ void __launch_bounds__(Cfg<N>::kCW*(N / 8)) col_kernel(double2* __restrict__ s,
-                                                                  const double* __restrict__ sym,
-                                                                  const double2* __restrict__ tw) {
-  using C = Cfg<N>;
+template <int N, int CW>
+__global__ void __launch_bounds__(CW*(N / 8)) col_kernel(double2* __restrict__ s, const double* __restrict__ sym,
+                                                         const double2* __restrict__ tw) {
+  using C = Cfg<N, 8, CW>;
   extern __shared__ double2 sm[];
   // Lanes interleave the kCW columns (team = column), so every warp-wide
   // global access covers kCW adjacent double2 of a few rows (coalesced); the
@@ -197,10 +199,10 @@ __global__ void __launch_bounds__(Cfg<N>::kCW*(N / 8)) col_kernel(double2* __res
 }
 
 // --------------------------------------------------------- fused RK stage --
-template <int N, int MODE>
+template <int N, int MODE, int T>
 __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
-  using C = Cfg<N>;
-  constexpr int T = C::kT, R = T + 2;
+  using C = Cfg<N, T>;
+  constexpr int R = T + 2;
   extern __shared__ double smd[];
   double* P = smd;                             // R x N inverse-FFT field
   double* X = P + R * N;                       // R x N stencil input
@@ -569,21 +571,31 @@ namespace {
 template <int N>
 struct Launch {
   using C = Cfg<N>;
+  // Small-block variants: when the 8-row / kCW-column grids would not fill
+  // the 148 SMs (PCG and line-search sweeps run one vector), use 2-row stage
+  // tiles and 1-column col CTAs (more, shorter CTAs: lower per-stage latency).
+  static constexpr int kSmallT = N >= 128 ? 2 : 8;
+  using CS = Cfg<N, kSmallT>;
+  static constexpr int kFill = 2 * 148;
+  static bool small_stage(int nvec) { return (N / C::kT) * nvec < kFill; }
+  static bool small_col(int nvec) { return ((N / 2) / C::kCW) * nvec < kFill; }
+  template <class K>
+  static void smem_attr(K k, size_t bytes) {
+    SDV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+  }
   static void setup() {
     static bool done = false;
     if (done) return;
-    SDV_CUDA(cudaFuncSetAttribute(stage_kernel<N, kModeTlm>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(C::kStageSmem)));
-    SDV_CUDA(cudaFuncSetAttribute(stage_kernel<N, kModeAdj>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(C::kStageSmem)));
-    SDV_CUDA(cudaFuncSetAttribute(stage_kernel<N, kModeNl>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(C::kStageSmem)));
-    SDV_CUDA(cudaFuncSetAttribute(col_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(C::kColSmem)));
-    SDV_CUDA(cudaFuncSetAttribute(row_fwd_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(C::kRowSmem)));
-    SDV_CUDA(cudaFuncSetAttribute(row_inv_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(C::kRowSmem)));
+    smem_attr(stage_kernel<N, kModeTlm, 8>, C::kStageSmem);
+    smem_attr(stage_kernel<N, kModeAdj, 8>, C::kStageSmem);
+    smem_attr(stage_kernel<N, kModeNl, 8>, C::kStageSmem);
+    smem_attr(stage_kernel<N, kModeTlm, kSmallT>, CS::kStageSmem);
+    smem_attr(stage_kernel<N, kModeAdj, kSmallT>, CS::kStageSmem);
+    smem_attr(stage_kernel<N, kModeNl, kSmallT>, CS::kStageSmem);
+    smem_attr(col_kernel<N, C::kCW>, C::kColSmem);
+    smem_attr(col_kernel<N, 1>, Cfg<N, 8, 1>::kColSmem);
+    smem_attr(row_fwd_kernel<N>, C::kRowSmem);
+    smem_attr(row_inv_kernel<N>, C::kRowSmem);
     done = true;
   }
   static void row_fwd(const double* f, double2* s, int nvec, cudaStream_t st) {
@@ -600,18 +612,28 @@ struct Launch {
   }
   static void col(double2* s, const double* sym, int nvec, cudaStream_t st) {
     setup();
-    dim3 g((N / 2) / C::kCW, nvec);
-    col_kernel<N><<<g, C::kCW * C::kTeam, C::kColSmem, st>>>(s, sym, twiddle_table(N));
+    if (small_col(nvec)) {
+      col_kernel<N, 1><<<dim3(N / 2, nvec), C::kTeam, Cfg<N, 8, 1>::kColSmem, st>>>(s, sym, twiddle_table(N));
+    } else {
+      dim3 g((N / 2) / C::kCW, nvec);
+      col_kernel<N, C::kCW><<<g, C::kCW * C::kTeam, C::kColSmem, st>>>(s, sym, twiddle_table(N));
+    }
     SDV_LAUNCH_CHECK();
+  }
+  template <int T>
+  static void stage_t(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
+    using CT = Cfg<N, T>;
+    dim3 g(N / T, nvec);
+    switch (mode) {
+      case kModeTlm: stage_kernel<N, kModeTlm, T><<<g, kThreads, CT::kStageSmem, st>>>(a); break;
+      case kModeAdj: stage_kernel<N, kModeAdj, T><<<g, kThreads, CT::kStageSmem, st>>>(a); break;
+      default: stage_kernel<N, kModeNl, T><<<g, kThreads, CT::kStageSmem, st>>>(a); break;
+    }
   }
   static void stage(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
     setup();
-    dim3 g(N / C::kT, nvec);
-    switch (mode) {
-      case kModeTlm: stage_kernel<N, kModeTlm><<<g, kThreads, C::kStageSmem, st>>>(a); break;
-      case kModeAdj: stage_kernel<N, kModeAdj><<<g, kThreads, C::kStageSmem, st>>>(a); break;
-      default: stage_kernel<N, kModeNl><<<g, kThreads, C::kStageSmem, st>>>(a); break;
-    }
+    if (small_stage(nvec)) stage_t<kSmallT>(mode, a, nvec, st);
+    else stage_t<8>(mode, a, nvec, st);
     SDV_LAUNCH_CHECK();
   }
 };
