@@ -498,8 +498,67 @@ void Problem::misfit_adjoint(const Trajectory& tr, const double* w, int s, doubl
 
 void Problem::gram_apply(const Trajectory& tr, const double* v, int s, double* hv) const {
   wy_.ensure(static_cast<size_t>(s) * m());
-  misfit_apply(tr, v, s, wy_.get());
-  misfit_adjoint(tr, wy_.get(), s, hv);
+  wstate_.ensure(static_cast<size_t>(s) * dim_);
+  ensure_work(s);
+  auto run = [&] {
+    misfit_apply(tr, v, s, wy_.get());
+    misfit_adjoint(tr, wy_.get(), s, hv);
+  };
+  // Small blocks are launch-latency bound (thousands of short kernels per
+  // sweep): capture the sweep once as a CUDA graph and replay it. The key is
+  // every pointer the captured launches bake in.
+  if (s > 8 || std::getenv("SDV_NO_GRAPHS")) {
+    run();
+    return;
+  }
+  const std::vector<const void*> key = {&tr,         tr.w.get(),   tr.p.get(),    v,          hv,
+                                        wy_.get(),   wstate_.get(), wa_.get(),    wx0_.get(), wx1_.get(),
+                                        ws0_.get(),  ws1_.get(),    reinterpret_cast<const void*>(static_cast<intptr_t>(s))};
+  GraphEntry* hit = nullptr;
+  for (auto& g : graphs_)
+    if (g.key == key) hit = &g;
+  if (hit && hit->exec) {
+    SDV_CUDA(cudaGraphLaunch(hit->exec, st_));
+    count_launch(hit->nodes);
+    return;
+  }
+  if (!hit) {  // first use: plain launches (lazy initialisation happens here)
+    if (graphs_.size() >= 8) {
+      if (graphs_.front().exec) cudaGraphExecDestroy(graphs_.front().exec);
+      graphs_.erase(graphs_.begin());
+    }
+    graphs_.push_back(GraphEntry{key, nullptr, 0});
+    run();
+    return;
+  }
+  cudaGraph_t graph = nullptr;
+  const unsigned long long before = g_launches;
+  SDV_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+  try {
+    run();
+  } catch (...) {
+    cudaStreamEndCapture(st_, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  SDV_CUDA(cudaStreamEndCapture(st_, &graph));
+  hit->nodes = g_launches - before;  // kernels per replay
+  g_launches = before;
+  SDV_CUDA(cudaGraphInstantiate(&hit->exec, graph, 0));
+  SDV_CUDA(cudaGraphDestroy(graph));
+  SDV_CUDA(cudaGraphLaunch(hit->exec, st_));
+  count_launch(hit->nodes);
+}
+
+void Problem::clear_graphs() const {
+  for (auto& g : graphs_)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  graphs_.clear();
+}
+
+Problem::~Problem() {
+  clear_graphs();
+  if (st_) cudaStreamDestroy(st_);
 }
 
 double Problem::evaluate(const Trajectory& tr, const double* d_z, double* d_ctrl_grad, double* d_lambda0) const {

@@ -93,6 +93,20 @@ class Problem {
   mutable DevBuf<double> wa_, wx0_, wx1_, wstate_, wy_;
   mutable DevBuf<double2> ws0_, ws1_;
   mutable int work_nvec_ = 0;
+  // CUDA graphs of small-block Gram sweeps (PCG / probes replay the same
+  // launch sequence on the same buffers every iteration).
+  struct GraphEntry {
+    std::vector<const void*> key;
+    cudaGraphExec_t exec = nullptr;
+    unsigned long long nodes = 0;
+  };
+  mutable std::vector<GraphEntry> graphs_;
+  void clear_graphs() const;
+
+ public:
+  ~Problem();
+  Problem(const Problem&) = delete;
+  Problem& operator=(const Problem&) = delete;
 };
 
 }  // namespace sdv
