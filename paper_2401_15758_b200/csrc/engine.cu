@@ -310,39 +310,78 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
   }
   ensure_work(nvec);
   const int n = d_.n, g = std::min(nvec, group());
-  double* xb[2] = {wx0_.get(), wx1_.get()};
+  const long long sdim = static_cast<long long>(n) * (n / 2);
   for (int v0 = 0; v0 < nvec; v0 += g) {
     const int gn = std::min(g, nvec - v0);
-    double* dst = state + v0 * dim_;
-    double2* s_cur = ws0_.get();
-    double2* s_nxt = ws1_.get();
-    bve_row_fwd(n, dst, s_cur, gn, st_);
-    count_launch();
+    std::vector<Lane> lanes = split_lanes(v0, gn);
+    for (auto& L : lanes) {
+      L.s_cur = ws0_.get() + L.woff * sdim;
+      L.s_nxt = ws1_.get() + L.woff * sdim;
+      bve_row_fwd(n, state + L.v0 * dim_, L.s_cur, L.cnt, L.st);
+      count_launch();
+    }
     for (int k = k0; k < k1; ++k) {
       for (int s = 0; s < 4; ++s) {
-        bve_col(n, s_cur, sym_p_.get(), gn, st_);
-        StageArgs a = bve_args(d_);
-        a.stage = s;
-        a.s_in = s_cur;
-        a.s_out = s_nxt;
-        a.x_in = s == 0 ? dst : xb[(s - 1) & 1];
-        a.x_out = s < 3 ? xb[s & 1] : nullptr;
-        a.d = dst;
-        a.acc = wa_.get();
-        a.base_w = tr.w.get() + (static_cast<long long>(k) * 4 + s) * dim_;
-        a.base_p = tr.p.get() + (static_cast<long long>(k) * 4 + s) * dim_;
-        bve_stage(n, kModeTlm, a, gn, st_);
-        count_launch(2);
-        std::swap(s_cur, s_nxt);
+        // interleave the lanes' launches so their kernels co-reside on SMs
+        for (auto& L : lanes) {
+          bve_col(n, L.s_cur, sym_p_.get(), L.cnt, L.st);
+          count_launch();
+        }
+        for (auto& L : lanes) {
+          double* dst = state + L.v0 * dim_;
+          double* xb[2] = {wx0_.get() + L.woff * dim_, wx1_.get() + L.woff * dim_};
+          StageArgs a = bve_args(d_);
+          a.stage = s;
+          a.s_in = L.s_cur;
+          a.s_out = L.s_nxt;
+          a.x_in = s == 0 ? dst : xb[(s - 1) & 1];
+          a.x_out = s < 3 ? xb[s & 1] : nullptr;
+          a.d = dst;
+          a.acc = wa_.get() + L.woff * dim_;
+          a.base_w = tr.w.get() + (static_cast<long long>(k) * 4 + s) * dim_;
+          a.base_p = tr.p.get() + (static_cast<long long>(k) * 4 + s) * dim_;
+          bve_stage(n, kModeTlm, a, L.cnt, L.st);
+          count_launch();
+          std::swap(L.s_cur, L.s_nxt);
+        }
       }
       if (y && (k + 1) % d_.spi == 0) {
         const int iv = (k + 1) / d_.spi - 1;
-        gather_obs(dst, dim_, idx_.get(), static_cast<int>(n_obs_), w + static_cast<long long>(iv) * n_obs_,
-                   y + v0 * m() + static_cast<long long>(iv) * n_obs_, m(), gn, st_);
-        count_launch();
+        for (auto& L : lanes) {
+          gather_obs(state + L.v0 * dim_, dim_, idx_.get(), static_cast<int>(n_obs_),
+                     w + static_cast<long long>(iv) * n_obs_, y + L.v0 * m() + static_cast<long long>(iv) * n_obs_,
+                     m(), L.cnt, L.st);
+          count_launch();
+        }
       }
     }
+    join_lanes(lanes);
   }
+}
+
+std::vector<Problem::Lane> Problem::split_lanes(int v0, int gn) const {
+  // Two concurrent lanes (streams) per group when it holds >= 2 vectors.
+  std::vector<Lane> lanes;
+  const bool two = gn >= 2 && !std::getenv("SDV_ONE_LANE");
+  if (!two) {
+    lanes.push_back(Lane{v0, gn, 0, st_});
+    return lanes;
+  }
+  if (!st2_) SDV_CUDA(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking));
+  if (!ev_fork_) SDV_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+  if (!ev_join_) SDV_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+  SDV_CUDA(cudaEventRecord(ev_fork_, st_));
+  SDV_CUDA(cudaStreamWaitEvent(st2_, ev_fork_, 0));
+  const int a = (gn + 1) / 2;
+  lanes.push_back(Lane{v0, a, 0, st_});
+  lanes.push_back(Lane{v0 + a, gn - a, a, st2_});
+  return lanes;
+}
+
+void Problem::join_lanes(const std::vector<Lane>& lanes) const {
+  if (lanes.size() < 2) return;
+  SDV_CUDA(cudaEventRecord(ev_join_, st2_));
+  SDV_CUDA(cudaStreamWaitEvent(st_, ev_join_, 0));
 }
 
 void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1, const double* y,
@@ -365,56 +404,67 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
   }
   ensure_work(nvec);
   const int n = d_.n, g = std::min(nvec, group());
-  double* qb[2] = {wx0_.get(), wx1_.get()};
+  const long long sdim = static_cast<long long>(n) * (n / 2);
   for (int v0 = 0; v0 < nvec; v0 += g) {
     const int gn = std::min(g, nvec - v0);
-    double* lam = state + v0 * dim_;
-    double* acc = wa_.get();
-    double2* s_cur = ws0_.get();
-    double2* s_nxt = ws1_.get();
+    std::vector<Lane> lanes = split_lanes(v0, gn);
+    for (auto& L : lanes) {
+      L.s_cur = ws0_.get() + L.woff * sdim;
+      L.s_nxt = ws1_.get() + L.woff * sdim;
+    }
     int qi = 0;
     bool first = true;
     for (int k = k1 - 1; k >= k0; --k) {
       if (y && (k + 1) % d_.spi == 0) {
         const int iv = (k + 1) / d_.spi - 1;
-        scatter_obs(first ? lam : acc, dim_, idx_.get(), static_cast<int>(n_obs_),
-                    w + static_cast<long long>(iv) * n_obs_, y + v0 * m() + static_cast<long long>(iv) * n_obs_, m(),
-                    gn, st_);
-        count_launch();
+        for (auto& L : lanes) {
+          double* lam = state + L.v0 * dim_;
+          double* acc = wa_.get() + L.woff * dim_;
+          scatter_obs(first ? lam : acc, dim_, idx_.get(), static_cast<int>(n_obs_),
+                      w + static_cast<long long>(iv) * n_obs_, y + L.v0 * m() + static_cast<long long>(iv) * n_obs_,
+                      m(), L.cnt, L.st);
+          count_launch();
+        }
       }
       for (int s = 3; s >= 0; --s) {
         const bool has_prev = !first;
-        if (has_prev) {
-          bve_col(n, s_cur, sym_p_.get(), gn, st_);
+        if (has_prev)
+          for (auto& L : lanes) {
+            bve_col(n, L.s_cur, sym_p_.get(), L.cnt, L.st);
+            count_launch();
+          }
+        for (auto& L : lanes) {
+          StageArgs a = bve_args(d_);
+          a.stage = s;
+          a.flags = has_prev ? kFlagHasPrev : 0;
+          a.s_in = L.s_cur;
+          a.s_out = L.s_nxt;
+          a.d = state + L.v0 * dim_;
+          a.acc = wa_.get() + L.woff * dim_;
+          a.q_in = (qi ? wx1_.get() : wx0_.get()) + L.woff * dim_;
+          a.q_out = (qi ? wx0_.get() : wx1_.get()) + L.woff * dim_;
+          a.base_w = tr.w.get() + (static_cast<long long>(k) * 4 + s) * dim_;
+          a.base_p = tr.p.get() + (static_cast<long long>(k) * 4 + s) * dim_;
+          bve_stage(n, kModeAdj, a, L.cnt, L.st);
           count_launch();
+          std::swap(L.s_cur, L.s_nxt);
         }
-        StageArgs a = bve_args(d_);
-        a.stage = s;
-        a.flags = has_prev ? kFlagHasPrev : 0;
-        a.s_in = s_cur;
-        a.s_out = s_nxt;
-        a.d = lam;
-        a.acc = acc;
-        a.q_in = qb[qi];
-        a.q_out = qb[qi ^ 1];
-        a.base_w = tr.w.get() + (static_cast<long long>(k) * 4 + s) * dim_;
-        a.base_p = tr.p.get() + (static_cast<long long>(k) * 4 + s) * dim_;
-        bve_stage(n, kModeAdj, a, gn, st_);
-        count_launch();
-        std::swap(s_cur, s_nxt);
         qi ^= 1;
         first = false;
       }
     }
-    bve_col(n, s_cur, sym_p_.get(), gn, st_);
-    StageArgs a = bve_args(d_);
-    a.flags = kFlagHasPrev | kFlagFinish;
-    a.s_in = s_cur;
-    a.d = lam;
-    a.acc = acc;
-    a.q_in = qb[qi];
-    bve_stage(n, kModeAdj, a, gn, st_);
-    count_launch(2);
+    for (auto& L : lanes) {
+      bve_col(n, L.s_cur, sym_p_.get(), L.cnt, L.st);
+      StageArgs a = bve_args(d_);
+      a.flags = kFlagHasPrev | kFlagFinish;
+      a.s_in = L.s_cur;
+      a.d = state + L.v0 * dim_;
+      a.acc = wa_.get() + L.woff * dim_;
+      a.q_in = (qi ? wx1_.get() : wx0_.get()) + L.woff * dim_;
+      bve_stage(n, kModeAdj, a, L.cnt, L.st);
+      count_launch(2);
+    }
+    join_lanes(lanes);
   }
 }
 
@@ -558,6 +608,9 @@ void Problem::clear_graphs() const {
 
 Problem::~Problem() {
   clear_graphs();
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
+  if (st2_) cudaStreamDestroy(st2_);
   if (st_) cudaStreamDestroy(st_);
 }
 

@@ -102,6 +102,19 @@ class Problem {
   };
   mutable std::vector<GraphEntry> graphs_;
   void clear_graphs() const;
+  // Concurrent lanes: a sweep group split over two streams so the stage and
+  // column kernels of the two halves co-reside on the SMs.
+  struct Lane {
+    int v0 = 0, cnt = 0;   // vectors [v0, v0+cnt) of the caller's block
+    long long woff = 0;    // vector offset inside the sweep workspace
+    cudaStream_t st = nullptr;
+    double2* s_cur = nullptr;
+    double2* s_nxt = nullptr;
+  };
+  std::vector<Lane> split_lanes(int v0, int gn) const;
+  void join_lanes(const std::vector<Lane>& lanes) const;
+  mutable cudaStream_t st2_ = nullptr;
+  mutable cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
 
  public:
   ~Problem();
