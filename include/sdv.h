@@ -33,7 +33,13 @@ extern "C" {
 #define SDV_ENUMERIC (-34)
 #define SDV_ECUDA (-5)
 
-enum { SDV_MODEL_BURGERS = 1, SDV_MODEL_BVE = 2 };
+/* SDV_MODEL_BURGERS_DIRICHLET: the reference's own Burgers (proj/src/burgers.cpp,
+ * n interior points, zero walls, RK3-TVD); requires SDV_PRIOR_LAPLACIAN. */
+enum { SDV_MODEL_BURGERS = 1, SDV_MODEL_BVE = 2, SDV_MODEL_BURGERS_DIRICHLET = 3 };
+/* SDV_PRIOR_FOURIER: B = sigma^2 C, Fourier-diagonal (control-variable form).
+ * SDV_PRIOR_LAPLACIAN: Gamma = (alpha I - beta Lap*)^{-2} on the Dirichlet grid,
+ * stencil scale 1 (proj/src/prior.cpp:9-62), x-space background term. */
+enum { SDV_PRIOR_FOURIER = 0, SDV_PRIOR_LAPLACIAN = 1 };
 enum { SDV_SKETCH_RANDSVD = 0, SDV_SKETCH_NYSTROM = 1, SDV_SKETCH_SINGLEVIEW = 2, SDV_SKETCH_LANCZOS = 3 };
 /* proj/include/sketchdav/fourdvar.hpp:91-98 */
 enum {
@@ -61,6 +67,9 @@ typedef struct {
   double prior_sigma;   /* B = sigma^2 C */
   double prior_length;  /* Gaussian correlation length */
   int block_group;      /* BVE: vectors per L2-resident sweep group (0 = auto) */
+  int prior_kind;       /* SDV_PRIOR_* */
+  double prior_alpha;   /* Laplacian prior: alpha */
+  double prior_beta;    /* Laplacian prior: beta */
 } sdv_problem_desc;
 
 const char* sdv_last_error(void);

@@ -85,13 +85,26 @@ std::vector<double> fourier_b_full(int n, int dims, double sigma, double len) {
 Problem::Problem(const ProblemDesc& d, long long n_obs, const long long* idx, const double* values,
                  const double* variances, const double* background)
     : d_(d), n_obs_(n_obs) {
-  if (d.model != kModelBurgers && d.model != kModelBVE) throw std::invalid_argument("problem: unknown model kind");
-  if (!is_pow2(d.n) || d.n < 32 || (d.model == kModelBurgers && d.n > 4096) || (d.model == kModelBVE && d.n > 512))
-    throw std::invalid_argument("problem: n must be a power of two (Burgers 32..4096, BVE 32..512)");
+  if (d.model != kModelBurgers && d.model != kModelBVE && d.model != kModelBurgers3)
+    throw std::invalid_argument("problem: unknown model kind");
+  if (d.model == kModelBurgers3) {
+    if (d.n < 3 || d.n > 4096) throw std::invalid_argument("problem: Dirichlet Burgers needs 3 <= n <= 4096");
+    if (d.prior_kind != kPriorLaplacian)
+      throw std::invalid_argument("problem: the Dirichlet Burgers model takes the Laplacian prior");
+  } else {
+    if (!is_pow2(d.n) || d.n < 32 || (d.model == kModelBurgers && d.n > 4096) || (d.model == kModelBVE && d.n > 512))
+      throw std::invalid_argument("problem: n must be a power of two (Burgers 32..4096, BVE 32..512)");
+    if (d.prior_kind != kPriorFourier)
+      throw std::invalid_argument("problem: periodic models take the Fourier-diagonal prior");
+  }
   if (!(d.nu >= 0.0) || !(d.dt > 0.0)) throw std::invalid_argument("problem: need nu >= 0 and dt > 0");
   if (d.n_t < 1 || d.spi < 1) throw std::invalid_argument("AssimilationProblem: need n_t >= 1 and steps_per_interval >= 1");
-  if (!(d.prior_sigma > 0.0) || !(d.prior_length > 0.0)) throw std::invalid_argument("problem: prior sigma/length must be positive");
-  dim_ = d.model == kModelBurgers ? d.n : static_cast<long long>(d.n) * d.n;
+  if (d.prior_kind == kPriorFourier && (!(d.prior_sigma > 0.0) || !(d.prior_length > 0.0)))
+    throw std::invalid_argument("problem: prior sigma/length must be positive");
+  if (d.prior_kind == kPriorLaplacian &&
+      (d.prior_alpha < 0.0 || d.prior_beta < 0.0 || (d.prior_alpha == 0.0 && d.prior_beta == 0.0)))
+    throw std::invalid_argument("PriorCovariance: need alpha, beta >= 0 with alpha + beta > 0");
+  dim_ = d.model == kModelBVE ? static_cast<long long>(d.n) * d.n : d.n;
   if (n_obs < 0 || n_obs > dim_) throw std::invalid_argument("AssimilationProblem: n_obs > n");
   long long prev = -1;
   for (long long k = 0; k < n_obs; ++k) {
@@ -117,7 +130,20 @@ Problem::Problem(const ProblemDesc& d, long long n_obs, const long long* idx, co
   rinv_.upload(m > 0 ? ri.data() : &zero, static_cast<size_t>(std::max<long long>(m, 1)), st_);
   background_.upload(background, static_cast<size_t>(dim_), st_);
   const int n = d.n;
-  if (d.model == kModelBurgers) {
+  if (d.prior_kind == kPriorLaplacian) {
+    // Tridiagonal1D(n, alpha + 2b, -b) pivots (proj/src/dirichlet.cpp:157-170,
+    // proj/src/prior.cpp:9-30 with stencil scale 1).
+    lap_b_ = d.prior_beta;
+    const double diag = d.prior_alpha + 2.0 * lap_b_, off = -lap_b_;
+    std::vector<double> piv(static_cast<size_t>(n));
+    double dd = diag;
+    for (int i = 0; i < n; ++i) {
+      if (!(dd > 0.0)) throw std::runtime_error("Tridiagonal1D: factorization failed");
+      piv[i] = dd;
+      dd = diag - off * off / dd;
+    }
+    pivot_.upload(piv.data(), piv.size(), st_);
+  } else if (d.model == kModelBurgers) {
     const std::vector<double> sb = fourier_b_full(n, 1, d.prior_sigma, d.prior_length);
     sym_b_.upload(sb.data(), sb.size(), st_);
   } else {
@@ -164,7 +190,7 @@ void Problem::ensure_work(int nvec) const {
 const double* Trajectory::state_at(int step) const {
   if (step < 0 || step > steps) throw std::invalid_argument("trajectory: step out of range");
   if (step == steps) return final.get();
-  return w.get() + static_cast<long long>(step) * 4 * prob->dim();
+  return w.get() + static_cast<long long>(step) * stages * prob->dim();
 }
 
 namespace {
@@ -173,8 +199,10 @@ BurgersArgs burgers_args(const ProblemDesc& d) {
   a.n = d.n;
   a.dt = d.dt;
   a.nu = d.nu;
-  a.c1 = 0.5 * d.n;
-  a.c2 = static_cast<double>(d.n) * d.n;
+  // periodic: dx = 1/n; Dirichlet: dx = 1/(n+1) (proj/src/burgers.cpp:57-58)
+  const int m = d.model == kModelBurgers3 ? d.n + 1 : d.n;
+  a.c1 = 0.5 * m;
+  a.c2 = static_cast<double>(m) * m;
   a.spi = d.spi;
   return a;
 }
@@ -191,6 +219,11 @@ StageArgs bve_args(const ProblemDesc& d) {
 }  // namespace
 
 void Problem::forward(const double* d_x0, int steps, double* d_out) const {
+  if (d_.model == kModelBurgers3) {
+    burgers3_fwd(burgers_args(d_), d_x0, nullptr, d_out, steps, st_);
+    count_launch();
+    return;
+  }
   if (d_.model == kModelBurgers) {
     burgers_fwd(burgers_args(d_), d_x0, nullptr, d_out, steps, st_);
     count_launch();
@@ -226,10 +259,14 @@ std::unique_ptr<Trajectory> Problem::linearize(const double* d_x0) const {
   auto tr = std::make_unique<Trajectory>();
   tr->prob = this;
   tr->steps = total_steps();
-  const long long st_elems = static_cast<long long>(tr->steps) * 4 * dim_;
+  tr->stages = d_.model == kModelBurgers3 ? 3 : 4;
+  const long long st_elems = static_cast<long long>(tr->steps) * tr->stages * dim_;
   tr->w.alloc(static_cast<size_t>(st_elems));
   tr->final.alloc(static_cast<size_t>(dim_));
-  if (d_.model == kModelBurgers) {
+  if (d_.model == kModelBurgers3) {
+    burgers3_fwd(burgers_args(d_), d_x0, tr->w.get(), tr->final.get(), tr->steps, st_);
+    count_launch();
+  } else if (d_.model == kModelBurgers) {
     burgers_fwd(burgers_args(d_), d_x0, tr->w.get(), tr->final.get(), tr->steps, st_);
     count_launch();
   } else {
@@ -274,6 +311,12 @@ std::unique_ptr<Trajectory> Problem::linearize(const double* d_x0) const {
 }
 
 void Problem::prior_sqrt(const double* in, double* out, int nvec) const {
+  if (d_.prior_kind == kPriorLaplacian) {
+    // Gamma^{1/2} = (alpha I - beta Lap*)^{-1}: tridiagonal solve per vector
+    thomas_solve(d_.n, -lap_b_, pivot_.get(), in, out, nvec, st_);
+    count_launch();
+    return;
+  }
   if (d_.model == kModelBurgers) {
     spectral1d(d_.n, in, out, sym_b_.get(), nvec, st_);
     count_launch();
@@ -294,7 +337,7 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
   if (k0 < 0 || k1 > tr.steps || k0 > k1) throw std::invalid_argument("trajectory: step range out of bounds");
   if (y && k0 != 0) throw std::invalid_argument("tlm: observation gathers need k0 == 0");
   if (nvec <= 0 || k0 == k1) return;
-  if (d_.model == kModelBurgers) {
+  if (d_.model == kModelBurgers || d_.model == kModelBurgers3) {
     BurgersArgs a = burgers_args(d_);
     a.base = tr.w.get();
     a.k0 = k0;
@@ -304,7 +347,10 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
     a.w = w;
     a.y = y;
     a.m = m();
-    burgers_tlm(a, state, nvec, st_);
+    if (d_.model == kModelBurgers3)
+      burgers3_tlm(a, state, nvec, st_);
+    else
+      burgers_tlm(a, state, nvec, st_);
     count_launch();
     return;
   }
@@ -388,7 +434,7 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
                   const double* w) const {
   if (k0 < 0 || k1 > tr.steps || k0 > k1) throw std::invalid_argument("trajectory: step range out of bounds");
   if (nvec <= 0 || k0 == k1) return;
-  if (d_.model == kModelBurgers) {
+  if (d_.model == kModelBurgers || d_.model == kModelBurgers3) {
     BurgersArgs a = burgers_args(d_);
     a.base = tr.w.get();
     a.k0 = k0;
@@ -398,7 +444,10 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
     a.w = w;
     a.y = const_cast<double*>(y);
     a.m = m();
-    burgers_adj(a, state, nvec, st_);
+    if (d_.model == kModelBurgers3)
+      burgers3_adj(a, state, nvec, st_);
+    else
+      burgers_adj(a, state, nvec, st_);
     count_launch();
     return;
   }
@@ -477,14 +526,17 @@ void Problem::probe_stage_kernels(const Trajectory& tr, int s, int stages, float
     SDV_CUDA(cudaMemcpyAsync(wstate_.get() + v * dim_, tr.w.get(), sizeof(double) * dim_, cudaMemcpyDeviceToDevice,
                              st_));
   double tot_stage = 0.0, tot_col = 0.0;
-  if (d_.model == kModelBurgers) {
-    const int steps = std::max(1, std::min(tr.steps, stages / 4));
+  if (d_.model == kModelBurgers || d_.model == kModelBurgers3) {
+    const int steps = std::max(1, std::min(tr.steps, stages / tr.stages));
     BurgersArgs a = burgers_args(d_);
     a.base = tr.w.get();
     a.k0 = 0;
     a.k1 = steps;
     SDV_CUDA(cudaEventRecord(ev[0], st_));
-    burgers_tlm(a, wstate_.get(), s, st_);
+    if (d_.model == kModelBurgers3)
+      burgers3_tlm(a, wstate_.get(), s, st_);
+    else
+      burgers_tlm(a, wstate_.get(), s, st_);
     SDV_CUDA(cudaEventRecord(ev[1], st_));
     SDV_CUDA(cudaEventSynchronize(ev[1]));
     float ms = 0;
@@ -614,10 +666,28 @@ Problem::~Problem() {
   if (st_) cudaStreamDestroy(st_);
 }
 
-double Problem::evaluate(const Trajectory& tr, const double* d_z, double* d_ctrl_grad, double* d_lambda0) const {
+void Problem::prior_inv_sqrt(const double* in, double* out, int nvec) const {
+  if (d_.prior_kind != kPriorLaplacian) throw std::invalid_argument("prior_inv_sqrt: only the Laplacian prior has one");
+  lap_inv_sqrt(d_.n, d_.prior_alpha, lap_b_, in, out, nvec, st_);
+  count_launch();
+}
+
+double Problem::evaluate(const Trajectory& tr, const double* d_z, double* d_ctrl_grad, double* d_lambda0,
+                         double* d_grad_x) const {
   const long long mm = m();
   DevBuf<double> innov(static_cast<size_t>(std::max<long long>(mm, 1))), winnov(innov.size()), sc(2),
       lam(static_cast<size_t>(dim_));
+  // x-space background term (proj/src/fourdvar.cpp:101-104): dxb = x0 - xb,
+  // ib = Gamma^{-1} dxb, cost_b = dxb . ib / 2.
+  DevBuf<double> dxb, ib;
+  if (xspace()) {
+    dxb.alloc(static_cast<size_t>(dim_));
+    ib.alloc(static_cast<size_t>(dim_));
+    SDV_CUDA(cudaMemcpyAsync(dxb.get(), tr.state_at(0), sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
+    dev_axpby(dim_, -1.0, background_.get(), 1.0, dxb.get(), st_);
+    prior_inv_sqrt(dxb.get(), lam.get(), 1);
+    prior_inv_sqrt(lam.get(), ib.get(), 1);
+  }
   for (int i = 1; i <= d_.n_t; ++i) {
     const long long o = static_cast<long long>(i - 1) * n_obs_;
     if (n_obs_ > 0) {
@@ -629,12 +699,18 @@ double Problem::evaluate(const Trajectory& tr, const double* d_z, double* d_ctrl
     }
   }
   dev_dot(innov.get(), winnov.get(), mm, sc.get(), st_);
-  if (d_z) dev_dot(d_z, d_z, dim_, sc.get() + 1, st_);
+  if (xspace()) dev_dot(dxb.get(), ib.get(), dim_, sc.get() + 1, st_);
+  else if (d_z) dev_dot(d_z, d_z, dim_, sc.get() + 1, st_);
   else dev_fill(1, 0.0, sc.get() + 1, st_);
   dev_fill(dim_, 0.0, lam.get(), st_);
   adj(tr, lam.get(), 1, 0, total_steps(), innov.get(), rinv_.get());
   if (d_lambda0) SDV_CUDA(cudaMemcpyAsync(d_lambda0, lam.get(), sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
-  if (d_ctrl_grad) {
+  if (xspace()) {
+    // g = Gamma^{-1}(x0 - xb) + lambda0; ctrl_grad = Gamma^{1/2} g
+    dev_axpby(dim_, 1.0, lam.get(), 1.0, ib.get(), st_);
+    if (d_grad_x) SDV_CUDA(cudaMemcpyAsync(d_grad_x, ib.get(), sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
+    if (d_ctrl_grad) prior_sqrt(ib.get(), d_ctrl_grad, 1);
+  } else if (d_ctrl_grad) {
     prior_sqrt(lam.get(), d_ctrl_grad, 1);
     if (d_z) dev_axpby(dim_, 1.0, d_z, 1.0, d_ctrl_grad, st_);
   }

@@ -14,7 +14,12 @@
 
 namespace sdv {
 
-enum ModelKind { kModelBurgers = 1, kModelBVE = 2 };
+// kModelBurgers3: the reference's own Dirichlet RK3-TVD Burgers (F3).
+enum ModelKind { kModelBurgers = 1, kModelBVE = 2, kModelBurgers3 = 3 };
+// kPriorFourier: B = sigma^2 C, Fourier-diagonal Gaussian (control-variable
+// background term). kPriorLaplacian: Gamma = (alpha I - beta Lap*)^{-2}
+// (proj/src/prior.cpp), x-space background term as the reference.
+enum PriorKind { kPriorFourier = 0, kPriorLaplacian = 1 };
 
 struct ProblemDesc {
   int model = kModelBurgers;
@@ -23,6 +28,8 @@ struct ProblemDesc {
   int n_t = 0, spi = 0;
   double prior_sigma = 0, prior_length = 0;
   int block_group = 0;  // vectors per BVE sweep group (0 = auto)
+  int prior_kind = kPriorFourier;
+  double prior_alpha = 0, prior_beta = 0;
 };
 
 class Problem;
@@ -31,6 +38,7 @@ class Problem;
 struct Trajectory {
   const Problem* prob = nullptr;
   int steps = 0;
+  int stages = 4;        // stored stage inputs per step (RK4: 4, RK3-TVD: 3)
   DevBuf<double> w;      // [steps][4][dim] stage inputs
   DevBuf<double> p;      // BVE: [steps][4][dim] stage streamfunctions
   DevBuf<double> final;  // [dim]
@@ -66,8 +74,14 @@ class Problem {
   void misfit_adjoint(const Trajectory& tr, const double* w, int s, double* z) const;
   void gram_apply(const Trajectory& tr, const double* v, int s, double* hv) const;
 
-  // cost (host), ctrl_grad = z + Gamma^{1/2} lambda0, lambda0 (device, may be null).
-  double evaluate(const Trajectory& tr, const double* d_z, double* d_ctrl_grad, double* d_lambda0) const;
+  // cost (host); ctrl_grad = Gamma^{1/2} g (control form: z + Gamma^{1/2} lambda0);
+  // lambda0; x-space gradient g = Gamma^{-1}(x0 - xb) + lambda0 (Laplacian
+  // prior only). Device outputs may be null.
+  double evaluate(const Trajectory& tr, const double* d_z, double* d_ctrl_grad, double* d_lambda0,
+                  double* d_grad_x = nullptr) const;
+  bool xspace() const { return d_.prior_kind == kPriorLaplacian; }
+  // Gamma^{-1/2} (Laplacian prior only).
+  void prior_inv_sqrt(const double* in, double* out, int nvec) const;
 
   // Timing probe (bench roofline): mean duration of the fused stage kernel and
   // the column kernel over `stages` TLM stages on a group of s vectors. For
@@ -88,6 +102,8 @@ class Problem {
   DevBuf<long long> idx_;
   DevBuf<double> values_, rinv_sqrt_, rinv_, background_;
   DevBuf<double> sym_b_, sym_p_;
+  DevBuf<double> pivot_;  // Laplacian prior: Thomas pivots
+  double lap_b_ = 0;      // beta * stencil scale
   double dt_ = 0;
   // sweep workspace (grown on demand)
   mutable DevBuf<double> wa_, wx0_, wx1_, wstate_, wy_;

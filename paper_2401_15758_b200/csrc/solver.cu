@@ -784,14 +784,18 @@ LSResult more_thuente(Phi&& phi, double f0, double g0, double t0, const LSConfig
 
 struct Eval {
   double cost = 0;
-  DevBuf<double> g;  // control-space gradient z + B^{1/2} lambda0
+  DevBuf<double> g;   // control-space gradient Gamma^{1/2} g
+  DevBuf<double> gx;  // x-space gradient (Laplacian prior only)
   std::unique_ptr<Trajectory> traj;
+  // the gradient the reference measures convergence on (fourdvar.cpp:131)
+  const double* conv() const { return gx.size() ? gx.get() : g.get(); }
 };
 Eval evaluate_at(const Problem& p, const double* x, const double* z) {
   Eval e;
   e.traj = p.linearize(x);
   e.g.alloc(static_cast<size_t>(p.dim()));
-  e.cost = p.evaluate(*e.traj, z, e.g.get(), nullptr);
+  if (p.xspace()) e.gx.alloc(static_cast<size_t>(p.dim()));
+  e.cost = p.evaluate(*e.traj, z, e.g.get(), nullptr, p.xspace() ? e.gx.get() : nullptr);
   return e;
 }
 double inf_norm(const double* d, long long n, cudaStream_t st) {
@@ -821,7 +825,8 @@ GNResult gn_solve(const Problem& p, const GNConfig& cfg) {
   Eval ev = evaluate_at(p, x.get(), z.get());
   ++c_fwd;
   ++c_adj;
-  const double g0 = inf_norm(ev.g.get(), n, st);
+  const bool xspace = p.xspace();
+  const double g0 = inf_norm(ev.conv(), n, st);
   if (g0 == 0.0) {
     result.analysis.resize(static_cast<size_t>(n));
     x.download(result.analysis.data(), static_cast<size_t>(n), st);
@@ -845,7 +850,7 @@ GNResult gn_solve(const Problem& p, const GNConfig& cfg) {
   DevBuf<double> rhs(static_cast<size_t>(n)), dxt(static_cast<size_t>(n)), dx(static_cast<size_t>(n)),
       tx(static_cast<size_t>(n)), tz(static_cast<size_t>(n));
   for (int k = 0; k < cfg.max_gn_iters; ++k) {
-    const double gnorm = inf_norm(ev.g.get(), n, st);
+    const double gnorm = inf_norm(ev.conv(), n, st);
     if (gnorm / g0 < cfg.grad_tol) {
       result.converged = true;
       break;
@@ -923,7 +928,11 @@ GNResult gn_solve(const Problem& p, const GNConfig& cfg) {
     c_tlm += a_on.applies;
     c_adj += a_on.adjoint_applies;
 
-    const double dphi0 = host_dot(ev.g.get(), dxt.get(), n, st);
+    // directional derivative: x-space g . dx, or control-space g~ . dxt
+    auto slope = [&](const Eval& e) {
+      return xspace ? host_dot(e.gx.get(), dx.get(), n, st) : host_dot(e.g.get(), dxt.get(), n, st);
+    };
+    const double dphi0 = slope(ev);
     std::map<double, Eval> trials;
     auto eval_step = [&](double a) {
       copy_dev(tx.get(), x.get(), n, st);
@@ -940,7 +949,7 @@ GNResult gn_solve(const Problem& p, const GNConfig& cfg) {
       auto phi = [&](double a) {
         auto it = trials.find(a);
         if (it == trials.end()) it = trials.emplace(a, eval_step(a)).first;
-        return std::make_pair(it->second.cost, host_dot(it->second.g.get(), dxt.get(), n, st));
+        return std::make_pair(it->second.cost, slope(it->second));
       };
       const LSResult ls = more_thuente(phi, ev.cost, dphi0, 1.0, LSConfig{});
       log.rec[5] = ls.trials;
@@ -986,7 +995,7 @@ GNResult gn_solve(const Problem& p, const GNConfig& cfg) {
     log.rec[15] = c_oadj;
     result.iterations.push_back(log);
   }
-  const double gf = inf_norm(ev.g.get(), n, st);
+  const double gf = inf_norm(ev.conv(), n, st);
   if (!result.line_search_failed && !result.converged) result.converged = gf / g0 < cfg.grad_tol;
   result.analysis.resize(static_cast<size_t>(n));
   x.download(result.analysis.data(), static_cast<size_t>(n), st);

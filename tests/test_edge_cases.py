@@ -32,6 +32,22 @@ def test_problem_validation_raises_invalid_argument(bad, msg):
         api.Problem(*_args(**bad))
 
 
+@pytest.mark.parametrize("model,kind,alpha,beta,n,msg", [
+    (3, 0, 0.5, 500.0, 399, "Laplacian prior"),       # Dirichlet Burgers needs the Laplacian prior
+    (1, 1, 0.5, 500.0, 64, "Fourier-diagonal"),       # periodic models take the Fourier prior
+    (3, 1, 0.0, 0.0, 399, "alpha \\+ beta > 0"),      # proj/src/prior.cpp:11-12
+    (3, 1, -1.0, 5.0, 399, "alpha, beta >= 0"),
+    (3, 1, 0.5, 500.0, 2, "3 <= n <= 4096"),
+])
+def test_prior_validation(model, kind, alpha, beta, n, msg):
+    from paper_2401_15758_b200 import api
+
+    a = list(_args(model=1, n=n, idx=(0, 1)))
+    a[0] = model
+    with pytest.raises(ValueError, match=msg):
+        api.Problem(*a, prior_kind=kind, prior_alpha=alpha, prior_beta=beta)
+
+
 @pytest.mark.gpu
 def test_tlm_exactly_homogeneous_in_powers_of_two(oracle, sdv):
     from paper_2401_15758_b200 import scenario
