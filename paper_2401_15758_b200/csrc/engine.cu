@@ -27,14 +27,12 @@ const double2* twiddle_table(int n) {
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(n);
   if (it != cache.end()) return it->second;
-  std::vector<double2> h(static_cast<size_t>(n));
-  for (int m = 0; m < n; ++m) {
-    const double ang = -2.0 * M_PI * static_cast<double>(m) / static_cast<double>(n);
-    h[m] = make_double2(std::cos(ang), std::sin(ang));
-  }
+  const int cnt = std::max(1, fft_twiddle_count(n));
+  std::vector<double2> h(static_cast<size_t>(cnt), make_double2(1.0, 0.0));
+  fft_build_twiddles(n, h.data(), [](double ang) { return make_double2(std::cos(ang), std::sin(ang)); });
   double2* d = nullptr;
-  SDV_CUDA(cudaMalloc(&d, sizeof(double2) * n));
-  SDV_CUDA(cudaMemcpy(d, h.data(), sizeof(double2) * n, cudaMemcpyHostToDevice));
+  SDV_CUDA(cudaMalloc(&d, sizeof(double2) * cnt));
+  SDV_CUDA(cudaMemcpy(d, h.data(), sizeof(double2) * cnt, cudaMemcpyHostToDevice));
   cache[n] = d;
   return d;
 }

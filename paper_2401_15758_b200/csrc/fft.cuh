@@ -93,7 +93,51 @@ struct FftPass {
   static constexpr int R = PASS < n8 ? 8 : (rem == 2 ? 4 : 2);
   static constexpr int NS = 1 << (3 * PASS);
   static constexpr bool LAST = PASS == NP - 1;
+  // Offset of this pass's twiddle block in the per-pass table (pass 0 has
+  // none; every pass before the last is radix 8).
+  static constexpr int tw_off() {
+    int off = 0, ns = 8;
+    for (int p = 1; p < PASS; ++p) {
+      off += 7 * ns;
+      ns *= 8;
+    }
+    return off;
+  }
+  static constexpr int kTwOff = tw_off();
 };
+
+// Per-pass twiddle table of a length-n transform: pass p >= 1 owns a block of
+// (R_p - 1) NS_p entries, entry (r-1) NS_p + k = exp(-2 pi i r k S_p / n),
+// S_p = n / (NS_p R_p). Lanes of a warp hold consecutive k, so each twiddle
+// load is one contiguous 16-byte-per-lane access (a table indexed by r k S
+// gathers from up to 32 cache lines per load and dominated the L1 traffic).
+// Values are bit-identical to exp(-2 pi i m / n) at m = r k S.
+inline int fft_twiddle_count(int n) {
+  int tot = 0, ns = 8, rest = n / 8;
+  while (rest > 1) {
+    const int r = rest >= 8 ? 8 : rest;
+    tot += (r - 1) * ns;
+    ns *= r;
+    rest /= r;
+  }
+  return tot;
+}
+template <class Cplx, class Make>
+void fft_build_twiddles(int n, Cplx* out, Make make) {
+  int off = 0, ns = 8, rest = n / 8;
+  while (rest > 1) {
+    const int r = rest >= 8 ? 8 : rest, s = n / (ns * r);
+    for (int rr = 1; rr < r; ++rr)
+      for (int k = 0; k < ns; ++k) {
+        const long m = static_cast<long>(rr) * k * s;
+        const double ang = -2.0 * 3.14159265358979323846 * static_cast<double>(m) / static_cast<double>(n);
+        out[off + (rr - 1) * ns + k] = make(ang);
+      }
+    off += (r - 1) * ns;
+    ns *= r;
+    rest /= r;
+  }
+}
 
 // One Stockham pass for team thread t: 8/R butterflies b = t + (N/8) q.
 // Input index of (q, r): b + r N/R; output index: (b - k) R + k + r NS.
@@ -106,13 +150,13 @@ __host__ __device__ __forceinline__ void fft_pass_compute(double2* v, int t, con
     const int b = t + T * q;
     const int k = b & (P::NS - 1);
     if (P::NS > 1) {
-      constexpr int S = N / (P::NS * R);
+      const double2* twp = tw + P::kTwOff + k;
 #pragma unroll
       for (int r = 1; r < R; ++r) {
 #ifdef __CUDA_ARCH__
-        v[q * R + r] = cmul_tw<INV>(v[q * R + r], __ldg(tw + r * k * S));
+        v[q * R + r] = cmul_tw<INV>(v[q * R + r], __ldg(twp + (r - 1) * P::NS));
 #else
-        v[q * R + r] = cmul_tw<INV>(v[q * R + r], tw[r * k * S]);
+        v[q * R + r] = cmul_tw<INV>(v[q * R + r], twp[(r - 1) * P::NS]);
 #endif
       }
     }

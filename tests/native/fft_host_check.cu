@@ -28,8 +28,8 @@ void run_pass(std::vector<double2>& a, const std::vector<double2>& tw) {
 
 template <int N>
 double check(bool inv) {
-  std::vector<double2> tw(N), x(N), y;
-  for (int m = 0; m < N; ++m) tw[m] = make_double2(std::cos(-2 * M_PI * m / N), std::sin(-2 * M_PI * m / N));
+  std::vector<double2> tw(std::max(1, fft_twiddle_count(N))), x(N), y;
+  fft_build_twiddles(N, tw.data(), [](double a) { return make_double2(std::cos(a), std::sin(a)); });
   for (int i = 0; i < N; ++i) x[i] = make_double2(std::sin(1.3 * i + 0.2), std::cos(0.7 * i * i + 1.0));
   y = x;
   if (inv) run_pass<N, true, 0>(y, tw);

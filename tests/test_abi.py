@@ -69,3 +69,16 @@ def test_product_config_specs_match_baseline():
     assert (c[3].n, c[3].steps, c[3].spi, c[3].rank) == (512, 800, 80, 110)
     assert (c[4].n, c[4].steps, c[4].spi, c[4].rank, c[4].growth) == (256, 400, 20, 10, 10)
     assert [len(scenario.obs_indices(s)) for s in c] == [64, 512, 1024, 4096, 4096]
+
+
+def test_fft_pass_math_host_check(tmp_path):
+    """The register-blocked Stockham passes of csrc/fft.cuh (with the per-pass
+    twiddle table) against a naive DFT for every supported length, on the host."""
+    import subprocess
+
+    exe = tmp_path / "fft_host_check"
+    src = os.path.join(ROOT, "tests", "native", "fft_host_check.cu")
+    subprocess.run(["/usr/local/cuda/bin/nvcc", "-O2", "-std=c++17", "-o", str(exe), src], check=True,
+                   capture_output=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout
