@@ -105,6 +105,19 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+// Cache-line prefetch of `rows` periodic rows starting at row y of a field
+// (one 128-byte line per thread-iteration): L1 for the shared base tiles the
+// stencil walks, L2 for the per-vector RK state it streams.
+template <int N, bool L1>
+__device__ __forceinline__ void prefetch_rows(const double* f, int y, int rows, int tid, int nt) {
+  constexpr int kLines = N / 16;  // 128-byte lines per row
+  for (int i = tid; i < rows * kLines; i += nt) {
+    const double* a = f + static_cast<long long>((y + i / kLines) & (N - 1)) * N + (i % kLines) * 16;
+    if (L1) asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+    else asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+  }
+}
+
 __device__ __forceinline__ void shift3(double w[3][3]) {
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -162,23 +175,18 @@ __global__ void __launch_bounds__(kThreads) row_inv_kernel(const double2* __rest
 // Column kx = 0 holds X(0) + i X(n/2) per row; both are real-input columns, so
 // the multiplier is applied through the Hermitian split
 //   Z'(ky) = (s0+sN)/2 Z(ky) + (s0-sN)/2 conj(Z(-ky)).
+// Body shared by col_kernel and the column-0 CTA of col_solve_kernel. All
+// threads of the CTA call it (barriers); inactive ones only synchronise.
 template <int N, int CW>
-__global__ void __launch_bounds__(CW*(N / 8)) col_kernel(double2* __restrict__ s, const double* __restrict__ sym,
-                                                         const double2* __restrict__ tw) {
+__device__ __forceinline__ void col_fft_body(double2* __restrict__ s, const double* __restrict__ sym,
+                                             const double2* __restrict__ tw, double2* sm, int kx0, int team, int t,
+                                             bool active, long long v) {
   using C = Cfg<N, 8, CW>;
-  extern __shared__ double2 sm[];
-  // Lanes interleave the kCW columns (team = column), so every warp-wide
-  // global access covers kCW adjacent double2 of a few rows (coalesced); the
-  // first forward pass reads global memory directly and the last inverse
-  // pass writes it back (no staging pass).
-  const int team = threadIdx.x % C::kCW, t = threadIdx.x / C::kCW;
-  const int kx0 = blockIdx.x * C::kCW;
-  const long long v = blockIdx.y;
   double2* col = s + v * N * (N / 2) + kx0 + team;
   double2* buf = sm + team * C::kColStride;
   auto ld_glob = [&](int i) { return col[static_cast<long long>(i) * (N / 2)]; };
   auto st_own = [&](int i, double2 z) { buf[fpad(i)] = z; };
-  fft_team<N, false>(buf, tw, t, true, ld_glob, st_own);
+  fft_team<N, false>(buf, tw, t, active, ld_glob, st_own);
   __syncthreads();
   const int kx = kx0 + team;
   const double* sk = sym + static_cast<long long>(kx) * N;
@@ -195,7 +203,129 @@ __global__ void __launch_bounds__(CW*(N / 8)) col_kernel(double2* __restrict__ s
     return make_double2(pp * z.x + mm * zm.x, pp * z.y - mm * zm.y);
   };
   auto st_glob = [&](int i, double2 z) { col[static_cast<long long>(i) * (N / 2)] = z; };
-  fft_team<N, true>(buf, tw, t, true, ld_mul, st_glob);
+  fft_team<N, true>(buf, tw, t, active, ld_mul, st_glob);
+}
+template <int N, int CW>
+__global__ void __launch_bounds__(CW*(N / 8)) col_kernel(double2* __restrict__ s, const double* __restrict__ sym,
+                                                         const double2* __restrict__ tw) {
+  extern __shared__ double2 sm[];
+  // Lanes interleave the kCW columns (team = column), so every warp-wide
+  // global access covers kCW adjacent double2 of a few rows (coalesced); the
+  // first forward pass reads global memory directly and the last inverse
+  // pass writes it back (no staging pass).
+  col_fft_body<N, CW>(s, sym, tw, sm, blockIdx.x * CW, threadIdx.x % CW, threadIdx.x / CW, true, blockIdx.y);
+}
+
+// ------------------------------------------------ column Poisson solve --
+// For each kx >= 1 the 5-point Poisson operator restricted to one x-Fourier
+// mode is the circulant (1/h^2)(d - S - S^-1) in y, d = 2 + 4 sin^2(pi kx/N),
+// S the cyclic row shift. With rho + 1/rho = d (rho < 1),
+//   (d - S - S^-1)^-1 = rho (1 - rho S^-1)^-1 (1 - rho S)^-1,
+// i.e. a forward first-order recurrence F_j = w_j + rho F_{j-1} followed by a
+// backward one G_j = F_j + rho G_{j+1}, both cyclic. This is the exact
+// inverse the y-FFT/multiply/inverse-y-FFT of col_kernel applies (same
+// operator, same eigenvalues mu(kx, ky)), at ~10 flops per point instead of
+// two 512-point FFTs, with coalesced row-segment access and no twiddles.
+// Each thread owns RPS = N/32 consecutive rows of one column in registers;
+// the 32 segment carries of a column are chained through shared memory, and
+// the cyclic closure uses 1/(1 - rho^N). tab[kx] = {rho, rho^RPS,
+// 1/(1 - rho^N), h^2 rho / N} (the 1/N is the unnormalised inverse x-FFT).
+// Column kx = 0 (packed X(0) + i X(N/2), singular at kx = 0) stays on the
+// FFT path: the grid's last CTA column runs col_kernel's body on it.
+template <int N>
+__global__ void __launch_bounds__(256, N >= 512 ? 2 : 3)
+    col_solve_kernel(double2* __restrict__ s, const double4* __restrict__ tab, const double* __restrict__ sym,
+                     const double2* __restrict__ tw) {
+  constexpr int CS = 8, SEG = 32, RPS = N / SEG;
+  if (blockIdx.x == gridDim.x - 1) {
+    extern __shared__ double2 sm[];
+    col_fft_body<N, 1>(s, sym, tw, sm, 0, 0, threadIdx.x, threadIdx.x < N / 8, blockIdx.y);
+    return;
+  }
+  __shared__ double2 car[2][CS][SEG];
+  const int c = threadIdx.x % CS, sg = threadIdx.x / CS;
+  const int kx = blockIdx.x * CS + c;
+  const bool live = kx != 0;
+  const long long v = blockIdx.y;
+  double2* col = s + v * N * (N / 2) + kx + static_cast<long long>(sg) * RPS * (N / 2);
+  const double4 tb = tab[kx];
+  const double rho = tb.x, rhoR = tb.y, clos = tb.z, scale = tb.w;
+  double2 x[RPS];
+#pragma unroll
+  for (int k = 0; k < RPS; ++k) x[k] = live ? col[static_cast<long long>(k) * (N / 2)] : make_double2(0.0, 0.0);
+  // forward local recurrence (zero carry-in)
+  double2 f = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int k = 0; k < RPS; ++k) {
+    f = make_double2(fma(rho, f.x, x[k].x), fma(rho, f.y, x[k].y));
+    x[k] = f;
+  }
+  car[0][c][sg] = f;
+  __syncthreads();
+  if (sg == 0 && live) {
+    // carries into each segment, then the cyclic closure F_{-1} = F_{N-1}
+    double2 C = make_double2(0.0, 0.0);
+#pragma unroll 1
+    for (int q = 0; q < SEG; ++q) {
+      const double2 L = car[0][c][q];
+      car[0][c][q] = C;
+      C = make_double2(fma(rhoR, C.x, L.x), fma(rhoR, C.y, L.y));
+    }
+    const double2 Fm = make_double2(C.x * clos, C.y * clos);
+    double pw = 1.0;
+#pragma unroll 1
+    for (int q = 0; q < SEG; ++q) {
+      const double2 a = car[0][c][q];
+      car[0][c][q] = make_double2(fma(pw, Fm.x, a.x), fma(pw, Fm.y, a.y));
+      pw *= rhoR;
+    }
+  }
+  __syncthreads();
+  {
+    const double2 cin = car[0][c][sg];
+    double pw = rho;
+#pragma unroll
+    for (int k = 0; k < RPS; ++k) {
+      x[k] = make_double2(fma(pw, cin.x, x[k].x), fma(pw, cin.y, x[k].y));
+      pw *= rho;
+    }
+  }
+  // backward local recurrence (zero carry-in from above)
+  double2 g = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int k = RPS - 1; k >= 0; --k) {
+    g = make_double2(fma(rho, g.x, x[k].x), fma(rho, g.y, x[k].y));
+    x[k] = g;
+  }
+  car[1][c][sg] = g;
+  __syncthreads();
+  if (sg == 0 && live) {
+    double2 D = make_double2(0.0, 0.0);
+#pragma unroll 1
+    for (int q = SEG - 1; q >= 0; --q) {
+      const double2 M = car[1][c][q];
+      car[1][c][q] = D;
+      D = make_double2(fma(rhoR, D.x, M.x), fma(rhoR, D.y, M.y));
+    }
+    const double2 G0 = make_double2(D.x * clos, D.y * clos);
+    double pw = 1.0;
+#pragma unroll 1
+    for (int q = SEG - 1; q >= 0; --q) {
+      const double2 a = car[1][c][q];
+      car[1][c][q] = make_double2(fma(pw, G0.x, a.x), fma(pw, G0.y, a.y));
+      pw *= rhoR;
+    }
+  }
+  __syncthreads();
+  if (!live) return;
+  const double2 cin = car[1][c][sg];
+  double pw = rho;
+#pragma unroll
+  for (int k = RPS - 1; k >= 0; --k) {
+    const double2 z = make_double2(fma(pw, cin.x, x[k].x), fma(pw, cin.y, x[k].y));
+    col[static_cast<long long>(k) * (N / 2)] = make_double2(scale * z.x, scale * z.y);
+    pw *= rho;
+  }
 }
 
 // --------------------------------------------------------- fused RK stage --
@@ -217,6 +347,24 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
   double2* fbuf = F + team * C::kPad;
   const bool has_prev = MODE != kModeAdj || (p.flags & kFlagHasPrev);
   const bool finish = MODE == kModeAdj && (p.flags & kFlagFinish);
+  const bool pf = !(p.flags & kFlagNoPrefetch);
+
+  // Prefetch what the later phases read, so it streams in under the inverse
+  // FFT: the stencil's first base tile into L1 (shared by the whole tile,
+  // walked row by row), the per-vector RK state and stencil input into L2.
+  if (pf) {
+    if (MODE == kModeTlm) {
+      prefetch_rows<N, true>(p.base_p, y0 - 1, R, tid, kThreads);
+      prefetch_rows<N, false>(p.x_in + off, y0 - 1, R, tid, kThreads);
+      if (p.stage <= 2) prefetch_rows<N, false>(p.d + off, y0, T, tid, kThreads);
+      if (p.stage >= 1) prefetch_rows<N, false>(p.acc + off, y0, T, tid, kThreads);
+    } else if (MODE == kModeAdj && !finish) {
+      prefetch_rows<N, true>(p.base_p, y0 - 1, R, tid, kThreads);
+      if (has_prev) prefetch_rows<N, false>(p.q_in + off, y0 - 1, R, tid, kThreads);
+      prefetch_rows<N, false>(p.acc + off, y0 - 1, R, tid, kThreads);
+      prefetch_rows<N, false>(p.d + off, y0 - 1, R, tid, kThreads);
+    }
+  }
 
   // Phase 1: inverse x-FFT of rows y0-1 .. y0+T -> P.
   if (has_prev && !(p.flags & kFlagSkipInvFft)) {
@@ -248,6 +396,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
     }
     cp_async_wait_all();
   } else {
+    if (pf && !finish) prefetch_rows<N, true>(p.base_w, y0 - 1, R, tid, kThreads);
     // lambda/mu combination of SURVEY.md B.1, batched kB elements per thread
     // (all loads issued before any dependent arithmetic).
     const double dt = p.dt;
@@ -406,14 +555,13 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
   };
   if (!(p.flags & kFlagSkipStencil)) {
     if (MODE == kModeTlm) {
+      // all A sweeps (base psi_b), then all B sweeps (base omega_b): one base
+      // tile is walked at a time, the other streams into L1 meanwhile
+      if (pf) prefetch_rows<N, true>(p.base_w, y0 - 1, R, tid, kThreads);
 #pragma unroll
-      for (int cc = 0; cc < C::kCPT; ++cc) {
-        double rc[C::kRPG];
-        sweep(cc, X, p.base_p, std::integral_constant<int, 0>{}, rc);
-        sweep(cc, P, p.base_w, std::integral_constant<int, 1>{}, rc);
+      for (int cc = 0; cc < C::kCPT; ++cc) sweep(cc, X, p.base_p, std::integral_constant<int, 0>{}, res[cc]);
 #pragma unroll
-        for (int q = 0; q < C::kRPG; ++q) res[cc][q] = rc[q];
-      }
+      for (int cc = 0; cc < C::kCPT; ++cc) sweep(cc, P, p.base_w, std::integral_constant<int, 1>{}, res[cc]);
     } else if (MODE == kModeAdj) {
       // one sweep, one smem window (a) and two prefetched base windows
 #pragma unroll 1
@@ -610,14 +758,38 @@ struct Launch {
     row_inv_kernel<N><<<g, kThreads, C::kRowSmem, st>>>(s, f, twiddle_table(N));
     SDV_LAUNCH_CHECK();
   }
+  template <int CW>
+  static void col_cw(double2* s, const double* sym, int nvec, cudaStream_t st) {
+    using CC = Cfg<N, 8, CW>;
+    static bool attr = false;
+    if (!attr) {
+      smem_attr(col_kernel<N, CW>, CC::kColSmem);
+      attr = true;
+    }
+    col_kernel<N, CW><<<dim3((N / 2) / CW, nvec), CW * CC::kTeam, CC::kColSmem, st>>>(s, sym, twiddle_table(N));
+    SDV_LAUNCH_CHECK();
+  }
   static void col(double2* s, const double* sym, int nvec, cudaStream_t st) {
     setup();
+    if constexpr (N >= 256) {
+      static const int cw = std::getenv("SDV_COL_CW") ? std::atoi(std::getenv("SDV_COL_CW")) : 0;
+      if (!small_col(nvec) && cw == 8) return col_cw<8>(s, sym, nvec, st);
+      if (!small_col(nvec) && cw == 16) return col_cw<16>(s, sym, nvec, st);
+    }
     if (small_col(nvec)) {
       col_kernel<N, 1><<<dim3(N / 2, nvec), C::kTeam, Cfg<N, 8, 1>::kColSmem, st>>>(s, sym, twiddle_table(N));
     } else {
       dim3 g((N / 2) / C::kCW, nvec);
       col_kernel<N, C::kCW><<<g, C::kCW * C::kTeam, C::kColSmem, st>>>(s, sym, twiddle_table(N));
     }
+    SDV_LAUNCH_CHECK();
+  }
+  // Poisson column pass: kx >= 1 by the recurrence solver, kx = 0 (packed,
+  // singular) by the FFT column kernel on that one column.
+  static void col_solve(double2* s, const double4* tab, const double* sym, int nvec, cudaStream_t st) {
+    setup();
+    col_solve_kernel<N><<<dim3((N / 2) / 8 + 1, nvec), 256, Cfg<N, 8, 1>::kColSmem, st>>>(s, tab, sym,
+                                                                                         twiddle_table(N));
     SDV_LAUNCH_CHECK();
   }
   template <int T>
@@ -659,6 +831,9 @@ void bve_row_inv(int n, const double2* s, double* f, int nvec, cudaStream_t st) 
 }
 void bve_col(int n, double2* s, const double* sym, int nvec, cudaStream_t st) {
   dispatch_n(n, [&](auto c) { Launch<decltype(c)::value>::col(s, sym, nvec, st); });
+}
+void bve_col_solve(int n, double2* s, const double4* tab, const double* sym, int nvec, cudaStream_t st) {
+  dispatch_n(n, [&](auto c) { Launch<decltype(c)::value>::col_solve(s, tab, sym, nvec, st); });
 }
 void bve_stage(int n, int mode, const StageArgs& a, int nvec, cudaStream_t st) {
   dispatch_n(n, [&](auto c) { Launch<decltype(c)::value>::stage(mode, a, nvec, st); });

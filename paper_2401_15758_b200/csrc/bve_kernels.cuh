@@ -12,7 +12,8 @@ enum StageFlags {
   // timing experiments only (probe): skip a phase, results are garbage
   kFlagSkipInvFft = 16,
   kFlagSkipStencil = 32,
-  kFlagSkipFwdFft = 64
+  kFlagSkipFwdFft = 64,
+  kFlagNoPrefetch = 128  // A/B timing of the tile prefetches
 };
 
 // Arguments of one fused RK stage launch over a group of vectors.
@@ -44,6 +45,10 @@ void bve_row_fwd(int n, const double* f, double2* s, int nvec, cudaStream_t st);
 void bve_row_inv(int n, const double2* s, double* f, int nvec, cudaStream_t st);
 void bve_col(int n, double2* s, const double* sym, int nvec, cudaStream_t st);
 void bve_stage(int n, int mode, const StageArgs& a, int nvec, cudaStream_t st);
+// Poisson column pass by cyclic first-order recurrences (kx >= 1) + the FFT
+// column kernel on the packed kx = 0 column; tab: [n/2] {rho, rho^(n/32),
+// 1/(1-rho^n), h^2 rho/n}; sym: the Poisson spectral symbol (column 0 only).
+void bve_col_solve(int n, double2* s, const double4* tab, const double* sym, int nvec, cudaStream_t st);
 
 void gather_obs(const double* f, long long dim, const long long* idx, int n_obs, const double* w, double* y,
                 long long m, int nvec, cudaStream_t st);

@@ -157,8 +157,31 @@ Problem::Problem(const ProblemDesc& d, long long n_obs, const long long* idx, co
       }
     sym_b_.upload(sb.data(), sb.size(), st_);
     sym_p_.upload(sp.data(), sp.size(), st_);
+    // recurrence constants per kx (see col_solve_kernel): d = 2 + 4 s^2,
+    // rho = 1 / (1 + 2 s^2 + 2 s sqrt(1 + s^2)) (the root < 1 of rho + 1/rho = d)
+    std::vector<double> tab(static_cast<size_t>(n / 2) * 4, 0.0);
+    for (int kx = 1; kx < n / 2; ++kx) {
+      const double sx = std::sin(M_PI * kx / n);
+      const double rho = 1.0 / (1.0 + 2.0 * sx * sx + 2.0 * sx * std::sqrt(1.0 + sx * sx));
+      tab[4 * kx + 0] = rho;
+      tab[4 * kx + 1] = std::pow(rho, n / 32);
+      tab[4 * kx + 2] = 1.0 / (1.0 - std::pow(rho, n));
+      tab[4 * kx + 3] = h * h * rho / n;
+    }
+    solve_tab_.upload(tab.data(), tab.size(), st_);
   }
   SDV_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Problem::poisson_col(double2* s, int nvec, cudaStream_t st) const {
+  static const bool fft = std::getenv("SDV_COL_FFT") != nullptr;
+  if (fft) {
+    bve_col(d_.n, s, sym_p_.get(), nvec, st);
+    count_launch();
+  } else {
+    bve_col_solve(d_.n, s, reinterpret_cast<const double4*>(solve_tab_.get()), sym_p_.get(), nvec, st);
+    count_launch();
+  }
 }
 
 int Problem::group() const {
@@ -238,7 +261,7 @@ void Problem::forward(const double* d_x0, int steps, double* d_out) const {
   double* xb[2] = {wx0_.get(), wx1_.get()};
   for (int k = 0; k < steps; ++k)
     for (int s = 0; s < 4; ++s) {
-      bve_col(n, s_cur, sym_p_.get(), 1, st_);
+      poisson_col(s_cur, 1, st_);
       StageArgs a = bve_args(d_);
       a.stage = s;
       a.s_in = s_cur;
@@ -248,7 +271,7 @@ void Problem::forward(const double* d_x0, int steps, double* d_out) const {
       a.d = u;
       a.acc = wa_.get();
       bve_stage(n, kModeNl, a, 1, st_);
-      count_launch(2);
+      count_launch();
       std::swap(s_cur, s_nxt);
     }
 }
@@ -280,7 +303,7 @@ std::unique_ptr<Trajectory> Problem::linearize(const double* d_x0) const {
     double* xb[2] = {wx0_.get(), wx1_.get()};
     for (int k = 0; k < tr->steps; ++k)
       for (int s = 0; s < 4; ++s) {
-        bve_col(n, s_cur, sym_p_.get(), 1, st_);
+        poisson_col(s_cur, 1, st_);
         StageArgs a = bve_args(d_);
         a.stage = s;
         a.s_in = s_cur;
@@ -292,7 +315,7 @@ std::unique_ptr<Trajectory> Problem::linearize(const double* d_x0) const {
         a.store_w = tr->w.get() + (static_cast<long long>(k) * 4 + s) * dim_;
         a.store_p = tr->p.get() + (static_cast<long long>(k) * 4 + s) * dim_;
         bve_stage(n, kModeNl, a, 1, st_);
-        count_launch(2);
+        count_launch();
         std::swap(s_cur, s_nxt);
       }
   }
@@ -367,10 +390,7 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
     for (int k = k0; k < k1; ++k) {
       for (int s = 0; s < 4; ++s) {
         // interleave the lanes' launches so their kernels co-reside on SMs
-        for (auto& L : lanes) {
-          bve_col(n, L.s_cur, sym_p_.get(), L.cnt, L.st);
-          count_launch();
-        }
+        for (auto& L : lanes) poisson_col(L.s_cur, L.cnt, L.st);
         for (auto& L : lanes) {
           double* dst = state + L.v0 * dim_;
           double* xb[2] = {wx0_.get() + L.woff * dim_, wx1_.get() + L.woff * dim_};
@@ -476,10 +496,7 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
       for (int s = 3; s >= 0; --s) {
         const bool has_prev = !first;
         if (has_prev)
-          for (auto& L : lanes) {
-            bve_col(n, L.s_cur, sym_p_.get(), L.cnt, L.st);
-            count_launch();
-          }
+          for (auto& L : lanes) poisson_col(L.s_cur, L.cnt, L.st);
         for (auto& L : lanes) {
           StageArgs a = bve_args(d_);
           a.stage = s;
@@ -501,7 +518,7 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
       }
     }
     for (auto& L : lanes) {
-      bve_col(n, L.s_cur, sym_p_.get(), L.cnt, L.st);
+      poisson_col(L.s_cur, L.cnt, L.st);
       StageArgs a = bve_args(d_);
       a.flags = kFlagHasPrev | kFlagFinish;
       a.s_in = L.s_cur;
@@ -509,7 +526,7 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
       a.acc = wa_.get() + L.woff * dim_;
       a.q_in = (qi ? wx1_.get() : wx0_.get()) + L.woff * dim_;
       bve_stage(n, kModeAdj, a, L.cnt, L.st);
-      count_launch(2);
+      count_launch();
     }
     join_lanes(lanes);
   }
@@ -553,7 +570,7 @@ void Problem::probe_stage_kernels(const Trajectory& tr, int s, int stages, float
     for (int q = 0; q < stages; ++q) {
       const int k = (q / 4) % tr.steps, sg = q % 4;
       SDV_CUDA(cudaEventRecord(ev[0], st_));
-      bve_col(n, s_cur, sym_p_.get(), s, st_);
+      poisson_col(s_cur, s, st_);
       SDV_CUDA(cudaEventRecord(ev[1], st_));
       StageArgs a = bve_args(d_);
       a.stage = sg;

@@ -102,6 +102,10 @@ class Problem {
   DevBuf<long long> idx_;
   DevBuf<double> values_, rinv_sqrt_, rinv_, background_;
   DevBuf<double> sym_b_, sym_p_;
+  DevBuf<double> solve_tab_;  // BVE: per-kx recurrence constants of the Poisson column solve
+  // Poisson column pass on row spectra (recurrence solver; SDV_COL_FFT=1 selects
+  // the y-FFT / multiply / inverse y-FFT kernel instead).
+  void poisson_col(double2* s, int nvec, cudaStream_t st) const;
   DevBuf<double> pivot_;  // Laplacian prior: Thomas pivots
   double lap_b_ = 0;      // beta * stencil scale
   double dt_ = 0;
