@@ -329,10 +329,12 @@ __global__ void __launch_bounds__(256, N >= 512 ? 2 : 3)
 }
 
 // --------------------------------------------------------- fused RK stage --
-template <int N, int MODE, int T>
+// ST: RK stage as a compile-time constant (TLM/ADJ; -1 = runtime p.stage).
+template <int N, int MODE, int T, int ST = -1>
 __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
   using C = Cfg<N, T>;
   constexpr int R = T + 2;
+  const int stage = ST >= 0 ? ST : p.stage;
   extern __shared__ double smd[];
   double* P = smd;                             // R x N inverse-FFT field
   double* X = P + R * N;                       // R x N stencil input
@@ -356,8 +358,8 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
     if (MODE == kModeTlm) {
       prefetch_rows<N, true>(p.base_p, y0 - 1, R, tid, kThreads);
       prefetch_rows<N, false>(p.x_in + off, y0 - 1, R, tid, kThreads);
-      if (p.stage <= 2) prefetch_rows<N, false>(p.d + off, y0, T, tid, kThreads);
-      if (p.stage >= 1) prefetch_rows<N, false>(p.acc + off, y0, T, tid, kThreads);
+      if (stage >= 1 && stage <= 2) prefetch_rows<N, false>(p.d + off, y0, T, tid, kThreads);
+      if (stage >= 1) prefetch_rows<N, false>(p.acc + off, y0, T, tid, kThreads);
     } else if (MODE == kModeAdj && !finish) {
       prefetch_rows<N, true>(p.base_p, y0 - 1, R, tid, kThreads);
       if (has_prev) prefetch_rows<N, false>(p.q_in + off, y0 - 1, R, tid, kThreads);
@@ -414,8 +416,8 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
         const int r = e / N, x = e % N;
         gg[u] = off + static_cast<long long>((y0 - 1 + r) & (N - 1)) * N + x;
         qv[u] = has_prev ? qin[gg[u]] : 0.0;
-        av[u] = (finish || p.stage <= 1 || (p.stage == 3 && has_prev)) ? accp[gg[u]] : 0.0;
-        lv[u] = (finish || (p.stage == 3 && has_prev)) ? 0.0 : lamp[gg[u]];
+        av[u] = (finish || stage <= 1 || (stage == 3 && has_prev)) ? accp[gg[u]] : 0.0;
+        lv[u] = (finish || (stage == 3 && has_prev)) ? 0.0 : lamp[gg[u]];
       }
 #pragma unroll
       for (int u = 0; u < kB; ++u) {
@@ -429,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
           continue;
         }
         double a;
-        switch (p.stage) {
+        switch (stage) {
           case 3: {
             const double lam = has_prev ? av[u] + mu : lv[u];
             if (owned && has_prev) lamp[gg[u]] = lam;
@@ -466,90 +468,88 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
   const int xt = tid % C::kNCT, rg = tid / C::kNCT;
   const int r0 = 1 + rg * C::kRPG;  // first owned smem row of this group
   double res[C::kCPT][C::kRPG] = {};
-  // Two sweeps per column strip, each with one shared-memory window (X or P)
-  // and one global base-field window whose next row is prefetched one step
-  // ahead (halves the live windows, keeps global loads in flight):
-  //   TLM  A: J(psi_b, X) + nu Lap X        B: + J(P, omega_b), RK4 update
-  //   ADJ  A: q = -J(psi_b, a) + nu Lap a   B: r = -J(a, omega_b)
-  //   NL   one smem-only sweep: J(P, X) + nu Lap X, RK4 update
+  // TLM: two sweeps per column strip, each with one shared-memory window
+  // (X or P) and one global base-field window (L1-prefetched):
+  //   A: J(psi_b, X) + nu Lap X          B: + J(P, omega_b), RK4 update
+  // Windows are 4-slot rings indexed by the (unrolled, compile-time) row, so
+  // advancing a row renames registers instead of moving them; owned-row
+  // global addresses are one base pointer plus compile-time row offsets.
+  // NL: one smem-only sweep J(P, X) + nu Lap X with the RK4 update.
+  // Global row j (relative to the first owned row of this thread) of a field;
+  // only j = -1 and j = kRPG can wrap periodically.
+  const long long grow0 = static_cast<long long>(y0 + r0 - 1) * N;
+  const long long grow_m = static_cast<long long>((y0 + r0 - 2) & (N - 1)) * N;
+  const long long grow_p = static_cast<long long>((y0 + r0 - 1 + C::kRPG) & (N - 1)) * N;
+  auto grow_off = [&](int j) { return j < 0 ? grow_m : (j >= C::kRPG ? grow_p : grow0 + static_cast<long long>(j) * N); };
   auto sweep = [&](int cc, const double* S, const double* G, auto pass_c, double(&rc)[C::kRPG]) {
     constexpr int pass = decltype(pass_c)::value;
-    {
-      const int x = xt + cc * C::kNCT;
-      const int xs[3] = {(x - 1) & (N - 1), x, (x + 1) & (N - 1)};
-      auto grow = [&](int r, double* w) {
-        const double* row = G + static_cast<long long>((y0 + r - 1) & (N - 1)) * N;
+    const int x = xt + cc * C::kNCT;
+    const int xm = (x - 1) & (N - 1), xp = (x + 1) & (N - 1);
+    const double* S0 = S + r0 * N;
+    double ws[4][3], wg[4][3];
+    auto srow = [&](int j, double* w) {
+      const double* row = S0 + j * N;
+      w[0] = row[xm];
+      w[1] = row[x];
+      w[2] = row[xp];
+    };
+    auto grow = [&](int j, double* w) {
+      const double* row = G + grow_off(j);
+      w[0] = __ldg(row + xm);
+      w[1] = __ldg(row + x);
+      w[2] = __ldg(row + xp);
+    };
+    // RK state of owned row j (pass B), prefetched one row ahead
+    const long long g0 = off + grow0 + x;
+    double dn[2] = {0.0, 0.0}, an[2] = {0.0, 0.0};
+    auto rkload = [&](int j) {  // (stage 0 reads d from the X tile instead)
+      if (stage >= 1 && stage <= 2) dn[j & 1] = p.d[g0 + static_cast<long long>(j) * N];
+      if (stage >= 1) an[j & 1] = p.acc[g0 + static_cast<long long>(j) * N];
+    };
+    srow(-1, ws[0]);
+    srow(0, ws[1]);
+    grow(-1, wg[0]);
+    grow(0, wg[1]);
+    grow(1, wg[2]);
+    if (pass == 1) rkload(0);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) w[c] = __ldg(row + xs[c]);
-      };
-      double ws[3][3], wg[3][3], gn[3];
-      double dn = 0.0, an = 0.0;  // prefetched RK state (TLM pass B)
-      const bool rk = MODE == kModeTlm && pass == 1;
-      auto rkload = [&](int r) {
-        const long long g = off + static_cast<long long>((y0 + r - 1) & (N - 1)) * N + x;
-        if (p.stage <= 2) dn = p.d[g];
-        if (p.stage >= 1) an = p.acc[g];
-      };
-#pragma unroll
-      for (int dy = 0; dy < 2; ++dy) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) ws[dy][c] = S[(r0 - 1 + dy) * N + xs[c]];
-        grow(r0 - 1 + dy, wg[dy]);
-      }
-      grow(r0 + 1, gn);
-      if (rk) rkload(r0);
-#pragma unroll
-      for (int q = 0; q < C::kRPG; ++q) {
-        const int r = r0 + q;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          ws[2][c] = S[(r + 1) * N + xs[c]];
-          wg[2][c] = gn[c];
+    for (int q = 0; q < C::kRPG; ++q) {
+      const int sa = q & 3, sb = (q + 1) & 3, sc = (q + 2) & 3, sd = (q + 3) & 3;
+      srow(q + 1, ws[sc]);
+      if (q + 2 <= C::kRPG) grow(q + 2, wg[sd]);
+      if (pass == 1 && q + 1 < C::kRPG) rkload(q + 1);
+      const double W[3][3] = {{ws[sa][0], ws[sa][1], ws[sa][2]},
+                              {ws[sb][0], ws[sb][1], ws[sb][2]},
+                              {ws[sc][0], ws[sc][1], ws[sc][2]}};
+      const double B[3][3] = {{wg[sa][0], wg[sa][1], wg[sa][2]},
+                              {wg[sb][0], wg[sb][1], wg[sb][2]},
+                              {wg[sc][0], wg[sc][1], wg[sc][2]}};
+      if (pass == 0) {
+        rc[q] = arakawa12(B, W) * js + nu * lap5(W) * ls;
+      } else {
+        const long long g = g0 + static_cast<long long>(q) * N;
+        const double kk = rc[q] + arakawa12(W, B) * js;
+        // stage 0: x_in is d itself, already in the X tile
+        const double dcur = stage == 0 ? X[(r0 + q) * N + x] : dn[q & 1];
+        const double acur = an[q & 1];
+        double out;
+        if (stage == 0) {
+          p.acc[g] = dcur + dt / 6.0 * kk;
+          out = dcur + 0.5 * dt * kk;
+          p.x_out[g] = out;
+        } else if (stage == 1) {
+          p.acc[g] = acur + dt / 3.0 * kk;
+          out = dcur + 0.5 * dt * kk;
+          p.x_out[g] = out;
+        } else if (stage == 2) {
+          p.acc[g] = acur + dt / 3.0 * kk;
+          out = dcur + dt * kk;
+          p.x_out[g] = out;
+        } else {
+          out = acur + dt / 6.0 * kk;
+          p.d[g] = out;
         }
-        if (q + 1 < C::kRPG) grow(r + 2, gn);
-        const double dcur = dn, acur = an;
-        if (rk && q + 1 < C::kRPG) rkload(r + 1);
-        const long long g = off + static_cast<long long>((y0 + r - 1) & (N - 1)) * N + x;
-        if (MODE == kModeTlm) {
-          if (pass == 0) {
-            rc[q] = arakawa12(wg, ws) * js + nu * lap5(ws) * ls;
-          } else {
-            const double kk = rc[q] + arakawa12(ws, wg) * js;
-            double out;
-            switch (p.stage) {
-              case 0:
-                p.acc[g] = dcur + dt / 6.0 * kk;
-                out = dcur + 0.5 * dt * kk;
-                p.x_out[g] = out;
-                break;
-              case 1:
-                p.acc[g] = acur + dt / 3.0 * kk;
-                out = dcur + 0.5 * dt * kk;
-                p.x_out[g] = out;
-                break;
-              case 2:
-                p.acc[g] = acur + dt / 3.0 * kk;
-                out = dcur + dt * kk;
-                p.x_out[g] = out;
-                break;
-              default:
-                out = acur + dt / 6.0 * kk;
-                p.d[g] = out;
-                break;
-            }
-            rc[q] = out;
-          }
-        } else {  // ADJ
-          if (pass == 0) p.q_out[g] = -arakawa12(wg, ws) * js + nu * lap5(ws) * ls;
-          else rc[q] = -arakawa12(ws, wg) * js;
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          ws[0][c] = ws[1][c];
-          ws[1][c] = ws[2][c];
-          wg[0][c] = wg[1][c];
-          wg[1][c] = wg[2][c];
-        }
+        rc[q] = out;
       }
     }
   };
@@ -734,12 +734,8 @@ struct Launch {
   static void setup() {
     static bool done = false;
     if (done) return;
-    smem_attr(stage_kernel<N, kModeTlm, 8>, C::kStageSmem);
-    smem_attr(stage_kernel<N, kModeAdj, 8>, C::kStageSmem);
-    smem_attr(stage_kernel<N, kModeNl, 8>, C::kStageSmem);
-    smem_attr(stage_kernel<N, kModeTlm, kSmallT>, CS::kStageSmem);
-    smem_attr(stage_kernel<N, kModeAdj, kSmallT>, CS::kStageSmem);
-    smem_attr(stage_kernel<N, kModeNl, kSmallT>, CS::kStageSmem);
+    stage_attrs<8>(std::make_integer_sequence<int, 4>{});
+    stage_attrs<kSmallT>(std::make_integer_sequence<int, 4>{});
     smem_attr(col_kernel<N, C::kCW>, C::kColSmem);
     smem_attr(col_kernel<N, 1>, Cfg<N, 8, 1>::kColSmem);
     smem_attr(row_fwd_kernel<N>, C::kRowSmem);
@@ -796,11 +792,30 @@ struct Launch {
   static void stage_t(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
     using CT = Cfg<N, T>;
     dim3 g(N / T, nvec);
-    switch (mode) {
-      case kModeTlm: stage_kernel<N, kModeTlm, T><<<g, kThreads, CT::kStageSmem, st>>>(a); break;
-      case kModeAdj: stage_kernel<N, kModeAdj, T><<<g, kThreads, CT::kStageSmem, st>>>(a); break;
-      default: stage_kernel<N, kModeNl, T><<<g, kThreads, CT::kStageSmem, st>>>(a); break;
+    const size_t sm = CT::kStageSmem;
+    if (mode == kModeNl) {
+      stage_kernel<N, kModeNl, T><<<g, kThreads, sm, st>>>(a);
+      return;
     }
+    // TLM / ADJ: the RK stage is a template constant (no per-point branches)
+    const bool tlm = mode == kModeTlm;
+    switch (a.stage) {
+      case 0: tlm ? stage_kernel<N, kModeTlm, T, 0><<<g, kThreads, sm, st>>>(a)
+                  : stage_kernel<N, kModeAdj, T, 0><<<g, kThreads, sm, st>>>(a); break;
+      case 1: tlm ? stage_kernel<N, kModeTlm, T, 1><<<g, kThreads, sm, st>>>(a)
+                  : stage_kernel<N, kModeAdj, T, 1><<<g, kThreads, sm, st>>>(a); break;
+      case 2: tlm ? stage_kernel<N, kModeTlm, T, 2><<<g, kThreads, sm, st>>>(a)
+                  : stage_kernel<N, kModeAdj, T, 2><<<g, kThreads, sm, st>>>(a); break;
+      default: tlm ? stage_kernel<N, kModeTlm, T, 3><<<g, kThreads, sm, st>>>(a)
+                   : stage_kernel<N, kModeAdj, T, 3><<<g, kThreads, sm, st>>>(a); break;
+    }
+  }
+  template <int T, int... S>
+  static void stage_attrs(std::integer_sequence<int, S...>) {
+    const size_t sm = Cfg<N, T>::kStageSmem;
+    (smem_attr(stage_kernel<N, kModeTlm, T, S>, sm), ...);
+    (smem_attr(stage_kernel<N, kModeAdj, T, S>, sm), ...);
+    smem_attr(stage_kernel<N, kModeNl, T>, sm);
   }
   static void stage(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
     setup();
