@@ -567,43 +567,52 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
 #pragma unroll 1
       for (int cc = 0; cc < C::kCPT; ++cc) {
         const int x = xt + cc * C::kNCT;
-        const int xs[3] = {(x - 1) & (N - 1), x, (x + 1) & (N - 1)};
-        auto grow = [&](const double* G, int r, double* w) {
-          const double* row = G + static_cast<long long>((y0 + r - 1) & (N - 1)) * N;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) w[c] = __ldg(row + xs[c]);
+        const int xm = (x - 1) & (N - 1), xp = (x + 1) & (N - 1);
+        const double* S0 = X + r0 * N;
+        auto srow = [&](int j, double* w) {
+          const double* row = S0 + j * N;
+          w[0] = row[xm];
+          w[1] = row[x];
+          w[2] = row[xp];
         };
-        double wa[3][3], bp[3][3], bw[3][3], pn[3], wn[3];
-#pragma unroll
-        for (int dy = 0; dy < 2; ++dy) {
-#pragma unroll
-          for (int c = 0; c < 3; ++c) wa[dy][c] = X[(r0 - 1 + dy) * N + xs[c]];
-          grow(p.base_p, r0 - 1 + dy, bp[dy]);
-          grow(p.base_w, r0 - 1 + dy, bw[dy]);
-        }
-        grow(p.base_p, r0 + 1, pn);
-        grow(p.base_w, r0 + 1, wn);
+        auto grow = [&](const double* G, int j, double* w) {
+          const double* row = G + grow_off(j);
+          w[0] = __ldg(row + xm);
+          w[1] = __ldg(row + x);
+          w[2] = __ldg(row + xp);
+        };
+        // 4-slot ring windows (row j in slot (j+1) & 3), see the TLM sweep
+        double wa[4][3], bp[4][3], bw[4][3];
+        srow(-1, wa[0]);
+        srow(0, wa[1]);
+        grow(p.base_p, -1, bp[0]);
+        grow(p.base_p, 0, bp[1]);
+        grow(p.base_p, 1, bp[2]);
+        grow(p.base_w, -1, bw[0]);
+        grow(p.base_w, 0, bw[1]);
+        grow(p.base_w, 1, bw[2]);
+        const long long g0 = off + grow0 + x;
 #pragma unroll
         for (int q = 0; q < C::kRPG; ++q) {
-          const int r = r0 + q;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            wa[2][c] = X[(r + 1) * N + xs[c]];
-            bp[2][c] = pn[c];
-            bw[2][c] = wn[c];
+          const int sa = q & 3, sb = (q + 1) & 3, sc = (q + 2) & 3, sd = (q + 3) & 3;
+          srow(q + 1, wa[sc]);
+          if (q + 2 <= C::kRPG) {
+            grow(p.base_p, q + 2, bp[sd]);
+            grow(p.base_w, q + 2, bw[sd]);
           }
-          if (q + 1 < C::kRPG) {
-            grow(p.base_p, r + 2, pn);
-            grow(p.base_w, r + 2, wn);
-          }
-          const long long g = off + static_cast<long long>((y0 + r - 1) & (N - 1)) * N + x;
-          p.q_out[g] = -arakawa12(bp, wa) * js + nu * lap5(wa) * ls;
-          const double out = -arakawa12(wa, bw) * js;
+          const double A[3][3] = {{wa[sa][0], wa[sa][1], wa[sa][2]},
+                                  {wa[sb][0], wa[sb][1], wa[sb][2]},
+                                  {wa[sc][0], wa[sc][1], wa[sc][2]}};
+          const double BP[3][3] = {{bp[sa][0], bp[sa][1], bp[sa][2]},
+                                   {bp[sb][0], bp[sb][1], bp[sb][2]},
+                                   {bp[sc][0], bp[sc][1], bp[sc][2]}};
+          const double BW[3][3] = {{bw[sa][0], bw[sa][1], bw[sa][2]},
+                                   {bw[sb][0], bw[sb][1], bw[sb][2]},
+                                   {bw[sc][0], bw[sc][1], bw[sc][2]}};
+          p.q_out[g0 + static_cast<long long>(q) * N] = -arakawa12(BP, A) * js + nu * lap5(A) * ls;
+          const double out = -arakawa12(A, BW) * js;
           if (cc == 0) res[0][q] = out;
           else res[C::kCPT - 1][q] = out;
-          shift3(wa);
-          shift3(bp);
-          shift3(bw);
         }
       }
     } else {
