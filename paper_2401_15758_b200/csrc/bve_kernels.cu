@@ -401,60 +401,58 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
     if (pf && !finish) prefetch_rows<N, true>(p.base_w, y0 - 1, R, tid, kThreads);
     // lambda/mu combination of SURVEY.md B.1, batched kB elements per thread
     // (all loads issued before any dependent arithmetic).
+    // Row-wise: each thread owns column pairs (16-byte loads/stores), row
+    // offsets are computed once per row (only the two halo rows wrap), and
+    // kRB rows of loads are issued before the dependent arithmetic.
     const double dt = p.dt;
-    const double* __restrict__ qin = p.q_in;
-    double* __restrict__ lamp = p.d;
-    double* __restrict__ accp = p.acc;
-    constexpr int kB = 4;
+    const double2* __restrict__ qin = reinterpret_cast<const double2*>(p.q_in);
+    double2* __restrict__ lamp = reinterpret_cast<double2*>(p.d);
+    double2* __restrict__ accp = reinterpret_cast<double2*>(p.acc);
+    const bool need_a = finish || stage <= 1 || (stage == 3 && has_prev);
+    const bool need_l = !(finish || (stage == 3 && has_prev));
+    constexpr int kRB = R % 5 == 0 ? 5 : (R % 2 == 0 ? 2 : 1);
+    const double2 z2 = make_double2(0.0, 0.0);
 #pragma unroll 1
-    for (int e0 = tid; e0 < R * N; e0 += kB * kThreads) {
-      double qv[kB], av[kB], lv[kB];
-      long long gg[kB];
+    for (int x2 = tid; x2 < N / 2; x2 += kThreads) {
+#pragma unroll 1
+      for (int rb = 0; rb < R; rb += kRB) {
+        double2 qv[kRB], av[kRB], lv[kRB];
+        long long go[kRB];
 #pragma unroll
-      for (int u = 0; u < kB; ++u) {
-        const int e = min(e0 + u * kThreads, R * N - 1);  // tail lanes redo the last element
-        const int r = e / N, x = e % N;
-        gg[u] = off + static_cast<long long>((y0 - 1 + r) & (N - 1)) * N + x;
-        qv[u] = has_prev ? qin[gg[u]] : 0.0;
-        av[u] = (finish || stage <= 1 || (stage == 3 && has_prev)) ? accp[gg[u]] : 0.0;
-        lv[u] = (finish || (stage == 3 && has_prev)) ? 0.0 : lamp[gg[u]];
-      }
+        for (int u = 0; u < kRB; ++u) {
+          const int r = rb + u;
+          go[u] = (off + static_cast<long long>((y0 - 1 + r) & (N - 1)) * N) / 2 + x2;
+          qv[u] = has_prev ? qin[go[u]] : z2;
+          av[u] = need_a ? accp[go[u]] : z2;
+          lv[u] = need_l ? lamp[go[u]] : z2;
+        }
 #pragma unroll
-      for (int u = 0; u < kB; ++u) {
-        const int e = e0 + u * kThreads;
-        if (e >= R * N) break;
-        const int r = e / N;
-        const bool owned = r >= 1 && r <= T;
-        const double mu = has_prev ? qv[u] + P[e] : 0.0;
-        if (finish) {
-          if (owned) lamp[gg[u]] = av[u] + mu;
-          continue;
+        for (int u = 0; u < kRB; ++u) {
+          const int r = rb + u;
+          const bool owned = r >= 1 && r <= T;
+          const double2 pp = reinterpret_cast<const double2*>(P + r * N)[x2];
+          const double2 mu = has_prev ? make_double2(qv[u].x + pp.x, qv[u].y + pp.y) : z2;
+          if (finish) {
+            if (owned) lamp[go[u]] = make_double2(av[u].x + mu.x, av[u].y + mu.y);
+            continue;
+          }
+          double2 a;
+          if (stage == 3) {
+            const double2 lam = has_prev ? make_double2(av[u].x + mu.x, av[u].y + mu.y) : lv[u];
+            if (owned && has_prev) lamp[go[u]] = lam;
+            a = make_double2(dt / 6.0 * lam.x, dt / 6.0 * lam.y);
+          } else if (stage == 2) {
+            if (owned) accp[go[u]] = make_double2(lv[u].x + mu.x, lv[u].y + mu.y);
+            a = make_double2(dt / 3.0 * lv[u].x + dt * mu.x, dt / 3.0 * lv[u].y + dt * mu.y);
+          } else if (stage == 1) {
+            if (owned) accp[go[u]] = make_double2(av[u].x + mu.x, av[u].y + mu.y);
+            a = make_double2(dt / 3.0 * lv[u].x + 0.5 * dt * mu.x, dt / 3.0 * lv[u].y + 0.5 * dt * mu.y);
+          } else {
+            if (owned) accp[go[u]] = make_double2(av[u].x + mu.x, av[u].y + mu.y);
+            a = make_double2(dt / 6.0 * lv[u].x + 0.5 * dt * mu.x, dt / 6.0 * lv[u].y + 0.5 * dt * mu.y);
+          }
+          reinterpret_cast<double2*>(X + r * N)[x2] = a;
         }
-        double a;
-        switch (stage) {
-          case 3: {
-            const double lam = has_prev ? av[u] + mu : lv[u];
-            if (owned && has_prev) lamp[gg[u]] = lam;
-            a = dt / 6.0 * lam;
-            break;
-          }
-          case 2: {
-            if (owned) accp[gg[u]] = lv[u] + mu;
-            a = dt / 3.0 * lv[u] + dt * mu;
-            break;
-          }
-          case 1: {
-            if (owned) accp[gg[u]] = av[u] + mu;
-            a = dt / 3.0 * lv[u] + 0.5 * dt * mu;
-            break;
-          }
-          default: {
-            if (owned) accp[gg[u]] = av[u] + mu;
-            a = dt / 6.0 * lv[u] + 0.5 * dt * mu;
-            break;
-          }
-        }
-        X[e] = a;
       }
     }
     if (finish) return;
