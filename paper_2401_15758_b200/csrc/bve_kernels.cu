@@ -791,6 +791,10 @@ struct Launch {
   // singular) by the FFT column kernel on that one column.
   static void col_solve(double2* s, const double4* tab, const double* sym, int nvec, cudaStream_t st) {
     setup();
+    // Small blocks (PCG / line-search sweeps, one vector): the solver's N/16+1
+    // CTAs per vector would leave most SMs idle; the 1-column FFT kernel has
+    // N/2 CTAs per vector.
+    if (small_col(nvec)) return col(s, sym, nvec, st);
     col_solve_kernel<N><<<dim3((N / 2) / 8 + 1, nvec), 256, Cfg<N, 8, 1>::kColSmem, st>>>(s, tab, sym,
                                                                                          twiddle_table(N));
     SDV_LAUNCH_CHECK();
