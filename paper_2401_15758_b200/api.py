@@ -81,6 +81,8 @@ class Problem:
         check(lib().sdv_problem_dims(self._h, dims.ctypes.data_as(I64)))
         self.n, self.m, self.n_obs, self.n_t, self.spi, self.total_steps = (int(x) for x in dims)
         self.background = bg.copy()
+        self.obs_indices = idx.copy()
+        self.obs_values = vals.reshape(self.n_t, self.n_obs).copy()
 
     @property
     def handle(self):

@@ -130,3 +130,29 @@ def test_step_range_validation(sdv):
         tr.adj_range(0, 11, np.ones(n))
     with pytest.raises(ValueError):
         tr.state_at(11)
+
+
+def test_reference_format_artifacts(tmp_path):
+    """CSV schemas of proj/src/harness.cpp:620-692 (headers, %.17g, CRLF)."""
+    import numpy as np
+
+    from paper_2401_15758_b200 import artifacts
+
+    class P:
+        n = 8
+        obs_indices = np.array([1, 5])
+        obs_values = np.array([[0.1, 0.2], [1.0 / 3.0, -2.5]])
+
+    log = np.zeros((2, 16))
+    log[0, :] = [0, 10.5, 2.0, 1.0, 7, 1, 1, 1, 12, 3.5, np.nan, 2, 9, 10, 30, 30]
+    log[1, :] = [1, 1.25, 0.5, 0.5, 5, 2, 1, 0, 12, np.nan, 1.5, 4, 15, 17, 30, 30]
+    res = {"log": log, "summary": np.array([1.0, 0.25, 12, 1, 0])}
+    artifacts.write_run(str(tmp_path), "exp", P, res, mode=1, method=0, rank=12)
+    obs = open(tmp_path / "observations.csv", "rb").read().decode()
+    assert obs.startswith("time_index,component,state_index,value\r\n1,0,1,0.10000000000000001\r\n")
+    it = open(tmp_path / "iterations.csv", "rb").read().decode().split("\r\n")
+    assert it[0] == ("k,cost,grad_inf_norm,step_size,pcg_iterations,pcg_converged,line_search_trials,"
+                     "sketch_recomputed,final_rank,kappa_sk,kappa_re,offline_tlm,offline_adj,fwd,tlm,adj")
+    assert it[1] == "0,10.5,2,1,7,true,1,true,12,3.5,nan,30,30,2,9,10"
+    sm = open(tmp_path / "summary.csv", "rb").read().decode().split("\r\n")
+    assert sm[1] == "exp,gn,SketchPrec,RandSVD,12,8,true,2,12,30,30,4,15,17,1,0.125,ok"
