@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gn", default="", help="also time full GN solves for these configs, e.g. 0,1,2,4 (or 'all')")
+    ap.add_argument("--window", type=int, default=0,
+                    help="profiling only (ncu launch lists): shorten the model window to this many RK4 steps "
+                         "(2 observation intervals); the reported line then names the window in config")
     return ap.parse_args()
 
 
@@ -276,8 +279,10 @@ def run_ours(args, world, rank, local):
     dist = dist_init(world)
     sdv.init(local)
     spec = scenario.CONFIGS[args.config]
+    if args.window:
+        spec = scenario.with_window(spec, steps=args.window, spi=max(1, args.window // 2))
     s = args.s or spec.rank
-    sc = scenario.build(args.config, block_group=args.group)
+    sc = scenario.build(spec, block_group=args.group)
     prob = sc.problem
     tr = prob.linearize(prob.background)
     n = prob.n
@@ -352,8 +357,16 @@ def run_ours(args, world, rank, local):
     achieved = alg_bytes / (dur / 1000.0) / 1e9
     b_hvp = algorithmic_bytes_per_hvp(ngrid, stages, s)
     step_achieved = value / world * b_hvp / 1e9
+    # measured DRAM bytes of this kernel per launch (ncu --set full capture in
+    # profiles/ncu_traffic.json, per vector x the probe's group), when profiled
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if spec.model == api.MODEL_BVE and os.path.exists(tf):
+        t = json.load(open(tf)).get("bve_stage_kernel_tlm", {})
+        if t.get("grid") == spec.n:
+            traffic = t["dram_bytes_per_vector"] * g
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": None, "kernel": kname, "kernel_ms": dur, "col_kernel_ms": ms_col,
+            "traffic": traffic, "kernel": kname, "kernel_ms": dur, "col_kernel_ms": ms_col,
             "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
             "step_model": {"B_HVP_bytes": b_hvp, "achieved_GBs": step_achieved, "frac": step_achieved / hbm,
                            "note": "SURVEY.md 8(d) streaming model: HVP/s x B_HVP per GPU"}}

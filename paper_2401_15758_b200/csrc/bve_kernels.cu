@@ -133,6 +133,8 @@ template <int N>
 __global__ void __launch_bounds__(kThreads) row_fwd_kernel(const double* __restrict__ f, double2* __restrict__ s,
                                                            const double2* __restrict__ tw) {
   using C = Cfg<N>;
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ double2 sm[];
   const int team = threadIdx.x / C::kTeam, t = threadIdx.x % C::kTeam;
   const int pair = blockIdx.x * C::kTeams + team;
@@ -154,6 +156,8 @@ template <int N>
 __global__ void __launch_bounds__(kThreads) row_inv_kernel(const double2* __restrict__ s, double* __restrict__ f,
                                                            const double2* __restrict__ tw) {
   using C = Cfg<N>;
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ double2 sm[];
   const int team = threadIdx.x / C::kTeam, t = threadIdx.x % C::kTeam;
   const int pair = blockIdx.x * C::kTeams + team;
@@ -209,6 +213,8 @@ template <int N, int CW>
 __global__ void __launch_bounds__(CW*(N / 8)) col_kernel(double2* __restrict__ s, const double* __restrict__ sym,
                                                          const double2* __restrict__ tw) {
   extern __shared__ double2 sm[];
+  pdl_trigger();
+  pdl_wait();
   // Lanes interleave the kCW columns (team = column), so every warp-wide
   // global access covers kCW adjacent double2 of a few rows (coalesced); the
   // first forward pass reads global memory directly and the last inverse
@@ -237,6 +243,8 @@ __global__ void __launch_bounds__(256, N >= 512 ? 2 : 3)
     col_solve_kernel(double2* __restrict__ s, const double4* __restrict__ tab, const double* __restrict__ sym,
                      const double2* __restrict__ tw) {
   constexpr int CS = 8, SEG = 32, RPS = N / SEG;
+  pdl_trigger();
+  pdl_wait();
   if (blockIdx.x == gridDim.x - 1) {
     extern __shared__ double2 sm[];
     col_fft_body<N, 1>(s, sym, tw, sm, 0, 0, threadIdx.x, threadIdx.x < N / 8, blockIdx.y);
@@ -350,6 +358,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
   const bool has_prev = MODE != kModeAdj || (p.flags & kFlagHasPrev);
   const bool finish = MODE == kModeAdj && (p.flags & kFlagFinish);
   const bool pf = !(p.flags & kFlagNoPrefetch);
+  pdl_trigger();
 
   // Prefetch what the later phases read, so it streams in under the inverse
   // FFT: the stencil's first base tile into L1 (shared by the whole tile,
@@ -367,6 +376,8 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
       prefetch_rows<N, false>(p.d + off, y0 - 1, R, tid, kThreads);
     }
   }
+
+  pdl_wait();  // everything below reads what the previous launch wrote
 
   // Phase 1: inverse x-FFT of rows y0-1 .. y0+T -> P.
   if (has_prev && !(p.flags & kFlagSkipInvFft)) {
@@ -707,6 +718,8 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
 __global__ void gather_obs_kernel(const double* __restrict__ f, long long dim, const long long* __restrict__ idx,
                                   int n_obs, const double* __restrict__ w, double* __restrict__ y, long long m,
                                   int nvec) {
+  pdl_trigger();
+  pdl_wait();
   const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (e >= static_cast<long long>(n_obs) * nvec) return;
   const int v = static_cast<int>(e / n_obs), k = static_cast<int>(e % n_obs);
@@ -715,6 +728,8 @@ __global__ void gather_obs_kernel(const double* __restrict__ f, long long dim, c
 __global__ void scatter_obs_kernel(double* __restrict__ f, long long dim, const long long* __restrict__ idx,
                                    int n_obs, const double* __restrict__ w, const double* __restrict__ y, long long m,
                                    int nvec) {
+  pdl_trigger();
+  pdl_wait();
   const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (e >= static_cast<long long>(n_obs) * nvec) return;
   const int v = static_cast<int>(e / n_obs), k = static_cast<int>(e % n_obs);
@@ -752,40 +767,22 @@ struct Launch {
   static void row_fwd(const double* f, double2* s, int nvec, cudaStream_t st) {
     setup();
     dim3 g(ceil_div(N / 2, C::kTeams), nvec);
-    row_fwd_kernel<N><<<g, kThreads, C::kRowSmem, st>>>(f, s, twiddle_table(N));
-    SDV_LAUNCH_CHECK();
+    launch_pdl(row_fwd_kernel<N>, g, kThreads, C::kRowSmem, st, f, s, twiddle_table(N));
   }
   static void row_inv(const double2* s, double* f, int nvec, cudaStream_t st) {
     setup();
     dim3 g(ceil_div(N / 2, C::kTeams), nvec);
-    row_inv_kernel<N><<<g, kThreads, C::kRowSmem, st>>>(s, f, twiddle_table(N));
-    SDV_LAUNCH_CHECK();
-  }
-  template <int CW>
-  static void col_cw(double2* s, const double* sym, int nvec, cudaStream_t st) {
-    using CC = Cfg<N, 8, CW>;
-    static bool attr = false;
-    if (!attr) {
-      smem_attr(col_kernel<N, CW>, CC::kColSmem);
-      attr = true;
-    }
-    col_kernel<N, CW><<<dim3((N / 2) / CW, nvec), CW * CC::kTeam, CC::kColSmem, st>>>(s, sym, twiddle_table(N));
-    SDV_LAUNCH_CHECK();
+    launch_pdl(row_inv_kernel<N>, g, kThreads, C::kRowSmem, st, s, f, twiddle_table(N));
   }
   static void col(double2* s, const double* sym, int nvec, cudaStream_t st) {
     setup();
-    if constexpr (N >= 256) {
-      static const int cw = std::getenv("SDV_COL_CW") ? std::atoi(std::getenv("SDV_COL_CW")) : 0;
-      if (!small_col(nvec) && cw == 8) return col_cw<8>(s, sym, nvec, st);
-      if (!small_col(nvec) && cw == 16) return col_cw<16>(s, sym, nvec, st);
-    }
     if (small_col(nvec)) {
-      col_kernel<N, 1><<<dim3(N / 2, nvec), C::kTeam, Cfg<N, 8, 1>::kColSmem, st>>>(s, sym, twiddle_table(N));
+      launch_pdl(col_kernel<N, 1>, dim3(N / 2, nvec), C::kTeam, Cfg<N, 8, 1>::kColSmem, st, s, sym,
+                 twiddle_table(N));
     } else {
-      dim3 g((N / 2) / C::kCW, nvec);
-      col_kernel<N, C::kCW><<<g, C::kCW * C::kTeam, C::kColSmem, st>>>(s, sym, twiddle_table(N));
+      launch_pdl(col_kernel<N, C::kCW>, dim3((N / 2) / C::kCW, nvec), C::kCW * C::kTeam, C::kColSmem, st, s, sym,
+                 twiddle_table(N));
     }
-    SDV_LAUNCH_CHECK();
   }
   // Poisson column pass: kx >= 1 by the recurrence solver, kx = 0 (packed,
   // singular) by the FFT column kernel on that one column.
@@ -795,30 +792,22 @@ struct Launch {
     // CTAs per vector would leave most SMs idle; the 1-column FFT kernel has
     // N/2 CTAs per vector.
     if (small_col(nvec)) return col(s, sym, nvec, st);
-    col_solve_kernel<N><<<dim3((N / 2) / 8 + 1, nvec), 256, Cfg<N, 8, 1>::kColSmem, st>>>(s, tab, sym,
-                                                                                         twiddle_table(N));
-    SDV_LAUNCH_CHECK();
+    launch_pdl(col_solve_kernel<N>, dim3((N / 2) / 8 + 1, nvec), 256, Cfg<N, 8, 1>::kColSmem, st, s, tab, sym,
+               twiddle_table(N));
   }
   template <int T>
   static void stage_t(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
     using CT = Cfg<N, T>;
-    dim3 g(N / T, nvec);
+    const dim3 g(N / T, nvec), b(kThreads);
     const size_t sm = CT::kStageSmem;
-    if (mode == kModeNl) {
-      stage_kernel<N, kModeNl, T><<<g, kThreads, sm, st>>>(a);
-      return;
-    }
+    if (mode == kModeNl) return launch_pdl(stage_kernel<N, kModeNl, T>, g, b, sm, st, a);
     // TLM / ADJ: the RK stage is a template constant (no per-point branches)
     const bool tlm = mode == kModeTlm;
     switch (a.stage) {
-      case 0: tlm ? stage_kernel<N, kModeTlm, T, 0><<<g, kThreads, sm, st>>>(a)
-                  : stage_kernel<N, kModeAdj, T, 0><<<g, kThreads, sm, st>>>(a); break;
-      case 1: tlm ? stage_kernel<N, kModeTlm, T, 1><<<g, kThreads, sm, st>>>(a)
-                  : stage_kernel<N, kModeAdj, T, 1><<<g, kThreads, sm, st>>>(a); break;
-      case 2: tlm ? stage_kernel<N, kModeTlm, T, 2><<<g, kThreads, sm, st>>>(a)
-                  : stage_kernel<N, kModeAdj, T, 2><<<g, kThreads, sm, st>>>(a); break;
-      default: tlm ? stage_kernel<N, kModeTlm, T, 3><<<g, kThreads, sm, st>>>(a)
-                   : stage_kernel<N, kModeAdj, T, 3><<<g, kThreads, sm, st>>>(a); break;
+      case 0: return launch_pdl(tlm ? stage_kernel<N, kModeTlm, T, 0> : stage_kernel<N, kModeAdj, T, 0>, g, b, sm, st, a);
+      case 1: return launch_pdl(tlm ? stage_kernel<N, kModeTlm, T, 1> : stage_kernel<N, kModeAdj, T, 1>, g, b, sm, st, a);
+      case 2: return launch_pdl(tlm ? stage_kernel<N, kModeTlm, T, 2> : stage_kernel<N, kModeAdj, T, 2>, g, b, sm, st, a);
+      default: return launch_pdl(tlm ? stage_kernel<N, kModeTlm, T, 3> : stage_kernel<N, kModeAdj, T, 3>, g, b, sm, st, a);
     }
   }
   template <int T, int... S>
@@ -832,7 +821,6 @@ struct Launch {
     setup();
     if (small_stage(nvec)) stage_t<kSmallT>(mode, a, nvec, st);
     else stage_t<8>(mode, a, nvec, st);
-    SDV_LAUNCH_CHECK();
   }
 };
 
@@ -868,15 +856,13 @@ void gather_obs(const double* f, long long dim, const long long* idx, int n_obs,
                 long long m, int nvec, cudaStream_t st) {
   const long long tot = static_cast<long long>(n_obs) * nvec;
   if (tot == 0) return;
-  gather_obs_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(f, dim, idx, n_obs, w, y, m, nvec);
-  SDV_LAUNCH_CHECK();
+  launch_pdl(gather_obs_kernel, ceil_div(tot, 256), 256, 0, st, f, dim, idx, n_obs, w, y, m, nvec);
 }
 void scatter_obs(double* f, long long dim, const long long* idx, int n_obs, const double* w, const double* y,
                  long long m, int nvec, cudaStream_t st) {
   const long long tot = static_cast<long long>(n_obs) * nvec;
   if (tot == 0) return;
-  scatter_obs_kernel<<<ceil_div(tot, 256), 256, 0, st>>>(f, dim, idx, n_obs, w, y, m, nvec);
-  SDV_LAUNCH_CHECK();
+  launch_pdl(scatter_obs_kernel, ceil_div(tot, 256), 256, 0, st, f, dim, idx, n_obs, w, y, m, nvec);
 }
 
 }  // namespace sdv
