@@ -223,6 +223,38 @@ __global__ void __launch_bounds__(CW*(N / 8)) col_kernel(double2* __restrict__ s
 }
 
 // ------------------------------------------------ column Poisson solve --
+// Cyclic carries of one column across its 32 segments (lane = segment q).
+// FWD: slot holds L_q, the zero-carry forward recurrence value at the last row
+// of segment q; it becomes the closed carry into q,
+//   C_q = sum_{p<q} rho^{RPS (q-1-p)} L_p + rho^{RPS q} F_{-1},
+//   F_{-1} = F_{N-1} = C_32 / (1 - rho^N)   (clos = 1/(1 - rho^N)).
+// BWD: the mirror image for the backward recurrence (carries from above).
+template <bool FWD>
+__device__ __forceinline__ void carry_scan(double2& slot, double rhoR, double clos, int lane) {
+  constexpr unsigned kAll = 0xffffffffu;
+  double A = rhoR, bx = slot.x, by = slot.y;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double Ap = FWD ? __shfl_up_sync(kAll, A, d) : __shfl_down_sync(kAll, A, d);
+    const double px = FWD ? __shfl_up_sync(kAll, bx, d) : __shfl_down_sync(kAll, bx, d);
+    const double py = FWD ? __shfl_up_sync(kAll, by, d) : __shfl_down_sync(kAll, by, d);
+    if (FWD ? lane >= d : lane + d < 32) {
+      bx = fma(A, px, bx);
+      by = fma(A, py, by);
+      A *= Ap;
+    }
+  }
+  const int end = FWD ? 31 : 0, first = FWD ? 0 : 31;
+  const double tx = __shfl_sync(kAll, bx, end) * clos, ty = __shfl_sync(kAll, by, end) * clos;
+  double cx = FWD ? __shfl_up_sync(kAll, bx, 1) : __shfl_down_sync(kAll, bx, 1);
+  double cy = FWD ? __shfl_up_sync(kAll, by, 1) : __shfl_down_sync(kAll, by, 1);
+  double ae = FWD ? __shfl_up_sync(kAll, A, 1) : __shfl_down_sync(kAll, A, 1);
+  if (lane == first) {
+    cx = cy = 0.0;
+    ae = 1.0;
+  }
+  slot = make_double2(fma(ae, tx, cx), fma(ae, ty, cy));
+}
 // For each kx >= 1 the 5-point Poisson operator restricted to one x-Fourier
 // mode is the circulant (1/h^2)(d - S - S^-1) in y, d = 2 + 4 sin^2(pi kx/N),
 // S the cyclic row shift. With rho + 1/rho = d (rho < 1),
@@ -270,24 +302,12 @@ __global__ void __launch_bounds__(256, N >= 512 ? 2 : 3)
   }
   car[0][c][sg] = f;
   __syncthreads();
-  if (sg == 0 && live) {
-    // carries into each segment, then the cyclic closure F_{-1} = F_{N-1}
-    double2 C = make_double2(0.0, 0.0);
-#pragma unroll 1
-    for (int q = 0; q < SEG; ++q) {
-      const double2 L = car[0][c][q];
-      car[0][c][q] = C;
-      C = make_double2(fma(rhoR, C.x, L.x), fma(rhoR, C.y, L.y));
-    }
-    const double2 Fm = make_double2(C.x * clos, C.y * clos);
-    double pw = 1.0;
-#pragma unroll 1
-    for (int q = 0; q < SEG; ++q) {
-      const double2 a = car[0][c][q];
-      car[0][c][q] = make_double2(fma(pw, Fm.x, a.x), fma(pw, Fm.y, a.y));
-      pw *= rhoR;
-    }
-  }
+  // Segment carries: warp w chains column w's 32 segments (lane = segment)
+  // with a Kogge-Stone scan of the affine maps C -> rho^RPS C + L.
+  const int wc = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const double4 tw4 = tab[blockIdx.x * CS + wc];
+  const bool wlive = blockIdx.x * CS + wc != 0;
+  if (wlive) carry_scan<true>(car[0][wc][lane], tw4.y, tw4.z, lane);
   __syncthreads();
   {
     const double2 cin = car[0][c][sg];
@@ -307,23 +327,7 @@ __global__ void __launch_bounds__(256, N >= 512 ? 2 : 3)
   }
   car[1][c][sg] = g;
   __syncthreads();
-  if (sg == 0 && live) {
-    double2 D = make_double2(0.0, 0.0);
-#pragma unroll 1
-    for (int q = SEG - 1; q >= 0; --q) {
-      const double2 M = car[1][c][q];
-      car[1][c][q] = D;
-      D = make_double2(fma(rhoR, D.x, M.x), fma(rhoR, D.y, M.y));
-    }
-    const double2 G0 = make_double2(D.x * clos, D.y * clos);
-    double pw = 1.0;
-#pragma unroll 1
-    for (int q = SEG - 1; q >= 0; --q) {
-      const double2 a = car[1][c][q];
-      car[1][c][q] = make_double2(fma(pw, G0.x, a.x), fma(pw, G0.y, a.y));
-      pw *= rhoR;
-    }
-  }
+  if (wlive) carry_scan<false>(car[1][wc][lane], tw4.y, tw4.z, lane);
   __syncthreads();
   if (!live) return;
   const double2 cin = car[1][c][sg];
