@@ -35,7 +35,11 @@ extern "C" {
 
 /* SDV_MODEL_BURGERS_DIRICHLET: the reference's own Burgers (proj/src/burgers.cpp,
  * n interior points, zero walls, RK3-TVD); requires SDV_PRIOR_LAPLACIAN. */
-enum { SDV_MODEL_BURGERS = 1, SDV_MODEL_BVE = 2, SDV_MODEL_BURGERS_DIRICHLET = 3 };
+enum { SDV_MODEL_BURGERS = 1, SDV_MODEL_BVE = 2, SDV_MODEL_BURGERS_DIRICHLET = 3, SDV_MODEL_BVE_DIRICHLET = 4 };
+/* SDV_MODEL_BVE_DIRICHLET: the reference's own barotropic-vorticity model
+ * (proj/src/bve.cpp: n = nx columns x ny rows, zero walls, beta-term 1/Ro,
+ * forcing sin(pi y), RK3-TVD, DST Poisson); requires SDV_PRIOR_LAPLACIAN (2-D,
+ * unscaled stencil) and the ny / reynolds / rossby fields. */
 /* SDV_PRIOR_FOURIER: B = sigma^2 C, Fourier-diagonal (control-variable form).
  * SDV_PRIOR_LAPLACIAN: Gamma = (alpha I - beta Lap*)^{-2} on the Dirichlet grid,
  * stencil scale 1 (proj/src/prior.cpp:9-62), x-space background term. */
@@ -70,6 +74,9 @@ typedef struct {
   int prior_kind;       /* SDV_PRIOR_* */
   double prior_alpha;   /* Laplacian prior: alpha */
   double prior_beta;    /* Laplacian prior: beta */
+  int ny;               /* SDV_MODEL_BVE_DIRICHLET: rows */
+  double reynolds;      /* SDV_MODEL_BVE_DIRICHLET: Re */
+  double rossby;        /* SDV_MODEL_BVE_DIRICHLET: Ro */
 } sdv_problem_desc;
 
 const char* sdv_last_error(void);

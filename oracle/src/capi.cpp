@@ -69,7 +69,9 @@ int oracle_gaussian_matrix(int64_t n, int64_t l, uint64_t seed, double* out) {
 int oracle_scenario_create_ex(int cfg, int steps, int spi) {
   int h = -1;
   const int rc = guard([&] {
-    auto s = std::make_unique<Scenario>(cfg == 100 ? make_reference_burgers_1_1() : make_config(cfg, steps, spi));
+    auto s = std::make_unique<Scenario>(cfg == 100   ? make_reference_burgers_1_1()
+                                        : cfg == 101 ? make_reference_bve_2()
+                                                     : make_config(cfg, steps, spi));
     std::lock_guard<std::mutex> l(g_mu);
     g_sc.push_back(std::move(s));
     h = static_cast<int>(g_sc.size()) - 1;

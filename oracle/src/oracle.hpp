@@ -512,6 +512,7 @@ struct Scenario {
 // cfg_id 0..4 = BASELINE.json configs; extra ids for reference presets.
 Scenario make_config(int cfg_id, int steps_override = -1, int spi_override = -1);
 Scenario make_reference_burgers_1_1();  // preset burgers_1_1 (Dirichlet RK3)
+Scenario make_reference_bve_2();        // preset bve_2 (Dirichlet BVE, RK3)
 Vec bve_truth_fixture_regen(int nx, int ny, double re, double ro, double dt, int steps,
                             uint64_t seed);
 Vec periodic_grf_truth(int n, uint64_t seed);  // spectrum ∝ k^4 exp(-(k/4)^2), rms 1

@@ -180,6 +180,61 @@ Scenario make_reference_burgers_1_1() {
   return sc;
 }
 
+// Preset bve_2 (proj/src/harness.cpp:285-309, scenario generation :432-527):
+// 64 x 129 Dirichlet BVE (RK3-TVD, Re 200, Ro 0.0016), dt 0.001225 split into
+// spi = 4 inner steps, n_t = 8, 16 x 16 sensor grid (:85-103), obs variance
+// 361, prior (alpha I - beta Lap*)^{-2} with alpha 0, beta 0.06 and unscaled
+// stencil, truth = the spun-up fixture field (600 steps, mix_seed(1234, 7)).
+Scenario make_reference_bve_2() {
+  Scenario sc;
+  sc.name = "bve_2";
+  const uint64_t master = 1234;
+  const int nx = 64, ny = 129, n_t = 8, spi = 4;
+  const double re = 200.0, ro = 0.0016, dt = 0.001225 / spi, var = 361.0;
+  AssimilationProblem& p = sc.problem;
+  p.model = std::make_shared<DirichletBVE>(nx, ny, re, ro, dt);
+  p.prior = LaplacianPrior::make_2d(nx, ny, 0.0, 0.06);
+  sc.truth0 = bve_truth_fixture_regen(nx, ny, re, ro, dt, 600, mix_seed(master, kSpinupStream));
+  std::vector<int64_t> idx;
+  for (int l = 1; l <= 16; ++l) {
+    const long long iy = std::llround(l * (ny + 1) / 17.0);
+    for (int k = 1; k <= 16; ++k) {
+      const long long ix = std::llround(k * (nx + 1) / 17.0);
+      idx.push_back((ix - 1) + static_cast<long long>(nx) * (iy - 1));
+    }
+  }
+  sc.truth_states.push_back(sc.truth0);
+  Vec x = sc.truth0;
+  for (int i = 1; i <= n_t; ++i) {
+    x = p.model->forward(x, spi);
+    sc.truth_states.push_back(x);
+  }
+  const int64_t no = static_cast<int64_t>(idx.size());
+  p.obs.indices = idx;
+  p.obs.values = Mat(no, n_t);
+  p.obs.variances = Mat(no, n_t);
+  for (auto& v : p.obs.variances.a) v = var;
+  for (int i = 0; i < n_t; ++i) {
+    const Vec noise = gaussian_vector(no, mix_seed(master, kObsStream + static_cast<uint64_t>(i)));
+    for (int64_t k = 0; k < no; ++k)
+      p.obs.values(k, i) = sc.truth_states[i + 1][idx[k]] + std::sqrt(var) * noise[k];
+  }
+  p.background = p.prior->sample_background(sc.truth0, mix_seed(master, kBackgroundStream));
+  p.n_t = n_t;
+  p.steps_per_interval = spi;
+  p.validate();
+  sc.gn.mode = SolveMode::SketchPrec;
+  sc.gn.sketch.method = SketchMethod::RandSVD;
+  sc.gn.sketch.rank = 192;
+  sc.gn.sketch.growth = 64;
+  sc.gn.sketch.eps_sketch = 1.5;
+  sc.gn.sketch.eps_reuse = 50.0;
+  sc.gn.max_gn_iters = 4;
+  sc.gn.pcg_max_iter = 4000;
+  sc.gn.sketch.seed = mix_seed(master, kSolverSketchStream);
+  return sc;
+}
+
 // proj/src/harness.cpp:119-170: seeded smooth field, scaled to max 50, spun up.
 Vec bve_truth_fixture_regen(int nx, int ny, double re, double ro, double dt, int steps, uint64_t seed) {
   const DirichletBVE model(nx, ny, re, ro, dt);

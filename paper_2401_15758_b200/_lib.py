@@ -25,7 +25,7 @@ class ProblemDesc(C.Structure):
     _fields_ = [("model", C.c_int), ("n", C.c_int), ("nu", C.c_double), ("dt", C.c_double), ("n_t", C.c_int),
                 ("steps_per_interval", C.c_int), ("prior_sigma", C.c_double), ("prior_length", C.c_double),
                 ("block_group", C.c_int), ("prior_kind", C.c_int), ("prior_alpha", C.c_double),
-                ("prior_beta", C.c_double)]
+                ("prior_beta", C.c_double), ("ny", C.c_int), ("reynolds", C.c_double), ("rossby", C.c_double)]
 
 
 class GNConfigC(C.Structure):

@@ -19,7 +19,7 @@ import numpy as np
 
 from ._lib import D, GNConfigC, I32, I64, ProblemDesc, check, lib
 
-MODEL_BURGERS, MODEL_BVE, MODEL_BURGERS_DIRICHLET = 1, 2, 3
+MODEL_BURGERS, MODEL_BVE, MODEL_BURGERS_DIRICHLET, MODEL_BVE_DIRICHLET = 1, 2, 3, 4
 PRIOR_FOURIER, PRIOR_LAPLACIAN = 0, 1
 RANDSVD, NYSTROM, SINGLEVIEW, LANCZOS = 0, 1, 2, 3
 MODES = {"SketchSolv": 0, "SketchPrec": 1, "SketchPrecA": 2, "PrecGamma": 3, "PrecLanczos": 4, "PrecALanczos": 5}
@@ -64,12 +64,15 @@ class Problem:
     model 3: the reference's Dirichlet RK3 Burgers with the Laplacian prior
     (prior_kind=1, prior_alpha, prior_beta; x-space background term as
     proj/src/fourdvar.cpp:92-132).
+    model 4: the reference's Dirichlet BVE (n = nx columns, ny rows, reynolds,
+    rossby; proj/src/bve.cpp) with the 2-D Laplacian prior.
     """
 
     def __init__(self, model, n, nu, dt, n_t, steps_per_interval, prior_sigma, prior_length, obs_indices, obs_values,
-                 obs_variances, background, block_group=0, prior_kind=0, prior_alpha=0.0, prior_beta=0.0):
+                 obs_variances, background, block_group=0, prior_kind=0, prior_alpha=0.0, prior_beta=0.0, ny=0,
+                 reynolds=0.0, rossby=0.0):
         self.desc = ProblemDesc(model, n, nu, dt, n_t, steps_per_interval, prior_sigma, prior_length, block_group,
-                                prior_kind, prior_alpha, prior_beta)
+                                prior_kind, prior_alpha, prior_beta, ny, reynolds, rossby)
         idx = np.ascontiguousarray(obs_indices, dtype=np.int64)
         vals = _f64(obs_values)
         var = _f64(obs_variances)

@@ -104,6 +104,9 @@ int sdv_problem_create(const sdv_problem_desc* desc, int64_t n_obs, const int64_
     d.prior_kind = desc->prior_kind;
     d.prior_alpha = desc->prior_alpha;
     d.prior_beta = desc->prior_beta;
+    d.ny = desc->ny;
+    d.reynolds = desc->reynolds;
+    d.rossby = desc->rossby;
     auto p = std::make_unique<sdv_problem>();
     static_assert(sizeof(long long) == sizeof(int64_t), "int64");
     p->p = std::make_unique<sdv::Problem>(d, n_obs, reinterpret_cast<const long long*>(idx), values, variances,

@@ -83,12 +83,18 @@ std::vector<double> fourier_b_full(int n, int dims, double sigma, double len) {
 Problem::Problem(const ProblemDesc& d, long long n_obs, const long long* idx, const double* values,
                  const double* variances, const double* background)
     : d_(d), n_obs_(n_obs) {
-  if (d.model != kModelBurgers && d.model != kModelBVE && d.model != kModelBurgers3)
+  if (d.model != kModelBurgers && d.model != kModelBVE && d.model != kModelBurgers3 && d.model != kModelBVE3)
     throw std::invalid_argument("problem: unknown model kind");
   if (d.model == kModelBurgers3) {
     if (d.n < 3 || d.n > 4096) throw std::invalid_argument("problem: Dirichlet Burgers needs 3 <= n <= 4096");
     if (d.prior_kind != kPriorLaplacian)
       throw std::invalid_argument("problem: the Dirichlet Burgers model takes the Laplacian prior");
+  } else if (d.model == kModelBVE3) {
+    // proj/src/bve.cpp:12-26 (BVEModel ctor)
+    if (d.n < 3 || d.ny < 3 || !(d.reynolds > 0.0) || !(d.rossby > 0.0) || d.n > 1024 || d.ny > 1024)
+      throw std::invalid_argument("BVEModel: invalid parameters (need 3 <= nx, ny <= 1024, Re, Ro > 0)");
+    if (d.prior_kind != kPriorLaplacian)
+      throw std::invalid_argument("problem: the Dirichlet BVE model takes the Laplacian prior");
   } else {
     if (!is_pow2(d.n) || d.n < 32 || (d.model == kModelBurgers && d.n > 4096) || (d.model == kModelBVE && d.n > 512))
       throw std::invalid_argument("problem: n must be a power of two (Burgers 32..4096, BVE 32..512)");
@@ -102,7 +108,8 @@ Problem::Problem(const ProblemDesc& d, long long n_obs, const long long* idx, co
   if (d.prior_kind == kPriorLaplacian &&
       (d.prior_alpha < 0.0 || d.prior_beta < 0.0 || (d.prior_alpha == 0.0 && d.prior_beta == 0.0)))
     throw std::invalid_argument("PriorCovariance: need alpha, beta >= 0 with alpha + beta > 0");
-  dim_ = d.model == kModelBVE ? static_cast<long long>(d.n) * d.n : d.n;
+  dim_ = d.model == kModelBVE ? static_cast<long long>(d.n) * d.n
+                              : (d.model == kModelBVE3 ? static_cast<long long>(d.n) * d.ny : d.n);
   if (n_obs < 0 || n_obs > dim_) throw std::invalid_argument("AssimilationProblem: n_obs > n");
   long long prev = -1;
   for (long long k = 0; k < n_obs; ++k) {
@@ -128,7 +135,27 @@ Problem::Problem(const ProblemDesc& d, long long n_obs, const long long* idx, co
   rinv_.upload(m > 0 ? ri.data() : &zero, static_cast<size_t>(std::max<long long>(m, 1)), st_);
   background_.upload(background, static_cast<size_t>(dim_), st_);
   const int n = d.n;
-  if (d.prior_kind == kPriorLaplacian) {
+  if (d.model == kModelBVE3) {
+    // proj/src/bve.cpp:12-26: dx = 1/(nx+1) on [0,1], dy = 2/(ny+1) on [-1,1]
+    const double dx = 1.0 / (n + 1), dy = 2.0 / (d.ny + 1);
+    b3_.nx = n;
+    b3_.ny = d.ny;
+    b3_.cx = 0.5 * (n + 1);
+    b3_.cy = 0.25 * (d.ny + 1);
+    b3_.lx = 1.0 / (dx * dx);
+    b3_.ly = 1.0 / (dy * dy);
+    b3_.inv_ro = 1.0 / d.rossby;
+    b3_.inv_re = 1.0 / d.reynolds;
+    b3_.dt = d.dt;
+    std::vector<double> f(static_cast<size_t>(d.ny));
+    for (int j = 0; j < d.ny; ++j) f[j] = std::sin(M_PI * (-1.0 + (j + 1) * dy));
+    forcing_.upload(f.data(), f.size(), st_);
+    b3_.forcing = forcing_.get();
+    poisson3_ = std::make_unique<DstSolver>(n, d.ny, 0.0, b3_.lx, b3_.ly, st_);
+    // Gamma^{1/2} = (alpha I + beta (-Lap*))^{-1}, unscaled stencil (proj/src/prior.cpp:32-51)
+    prior3_ = std::make_unique<DstSolver>(n, d.ny, d.prior_alpha, d.prior_beta, d.prior_beta, st_);
+    lap_b_ = d.prior_beta;
+  } else if (d.prior_kind == kPriorLaplacian) {
     // Tridiagonal1D(n, alpha + 2b, -b) pivots (proj/src/dirichlet.cpp:157-170,
     // proj/src/prior.cpp:9-30 with stencil scale 1).
     lap_b_ = d.prior_beta;
@@ -250,6 +277,24 @@ void Problem::forward(const double* d_x0, int steps, double* d_out) const {
     count_launch();
     return;
   }
+  if (d_.model == kModelBVE3) {
+    // RK3-TVD (proj/src/bve.cpp:84-101): stage s solves psi_s = P(w_s), then
+    // w_{s+1} = combination(u, w_s, rhs(w_s, psi_s))
+    bve3_work(1);
+    double* u = b3w_[0].get();
+    SDV_CUDA(cudaMemcpyAsync(u, d_x0, sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
+    double* ws[3] = {u, b3w_[1].get(), b3w_[2].get()};
+    double* ps = b3w_[3].get();
+    for (int k = 0; k < steps; ++k)
+      for (int s = 0; s < 3; ++s) {
+        poisson3_->solve(ws[s], ps, 1);
+        bve3_nl_stage(b3_, s, u, ws[s], ps, s < 2 ? ws[s + 1] : b3w_[4].get(), 1, st_);
+        count_launch(2);  // DST scale + stage (the 4 GEMMs are cuBLAS)
+        if (s == 2) SDV_CUDA(cudaMemcpyAsync(u, b3w_[4].get(), sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
+      }
+    SDV_CUDA(cudaMemcpyAsync(d_out, u, sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
+    return;
+  }
   ensure_work(1);
   const int n = d_.n;
   double* u = d_out;
@@ -280,11 +325,29 @@ std::unique_ptr<Trajectory> Problem::linearize(const double* d_x0) const {
   auto tr = std::make_unique<Trajectory>();
   tr->prob = this;
   tr->steps = total_steps();
-  tr->stages = d_.model == kModelBurgers3 ? 3 : 4;
+  tr->stages = (d_.model == kModelBurgers3 || d_.model == kModelBVE3) ? 3 : 4;
   const long long st_elems = static_cast<long long>(tr->steps) * tr->stages * dim_;
   tr->w.alloc(static_cast<size_t>(st_elems));
   tr->final.alloc(static_cast<size_t>(dim_));
-  if (d_.model == kModelBurgers3) {
+  if (d_.model == kModelBVE3) {
+    // stored per stage: w_s (stage input) and psi_s = P(w_s); the reference's
+    // StageFields ox, oy, px, py are their derivatives (proj/src/bve.cpp:171-182),
+    // recomputed in the TLM/ADJ kernels
+    tr->p.alloc(static_cast<size_t>(st_elems));
+    bve3_work(1);
+    double* u = tr->final.get();
+    SDV_CUDA(cudaMemcpyAsync(u, d_x0, sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
+    for (int k = 0; k < tr->steps; ++k) {
+      double* wk = tr->w.get() + static_cast<long long>(k) * 3 * dim_;
+      double* pk = tr->p.get() + static_cast<long long>(k) * 3 * dim_;
+      SDV_CUDA(cudaMemcpyAsync(wk, u, sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
+      for (int s = 0; s < 3; ++s) {
+        poisson3_->solve(wk + s * dim_, pk + s * dim_, 1);
+        bve3_nl_stage(b3_, s, wk, wk + s * dim_, pk + s * dim_, s < 2 ? wk + (s + 1) * dim_ : u, 1, st_);
+        count_launch(2);  // DST scale + stage (the 4 GEMMs are cuBLAS)
+      }
+    }
+  } else if (d_.model == kModelBurgers3) {
     burgers3_fwd(burgers_args(d_), d_x0, tr->w.get(), tr->final.get(), tr->steps, st_);
     count_launch();
   } else if (d_.model == kModelBurgers) {
@@ -332,6 +395,11 @@ std::unique_ptr<Trajectory> Problem::linearize(const double* d_x0) const {
 }
 
 void Problem::prior_sqrt(const double* in, double* out, int nvec) const {
+  if (d_.model == kModelBVE3) {
+    prior3_->solve(in, out, nvec);  // DirichletSolver2D(nx, ny, alpha, beta, beta)
+    count_launch();
+    return;
+  }
   if (d_.prior_kind == kPriorLaplacian) {
     // Gamma^{1/2} = (alpha I - beta Lap*)^{-1}: tridiagonal solve per vector
     thomas_solve(d_.n, -lap_b_, pivot_.get(), in, out, nvec, st_);
@@ -358,6 +426,7 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
   if (k0 < 0 || k1 > tr.steps || k0 > k1) throw std::invalid_argument("trajectory: step range out of bounds");
   if (y && k0 != 0) throw std::invalid_argument("tlm: observation gathers need k0 == 0");
   if (nvec <= 0 || k0 == k1) return;
+  if (d_.model == kModelBVE3) return bve3_tlm(tr, state, nvec, k0, k1, y, w);
   if (d_.model == kModelBurgers || d_.model == kModelBurgers3) {
     BurgersArgs a = burgers_args(d_);
     a.base = tr.w.get();
@@ -452,6 +521,7 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
                   const double* w) const {
   if (k0 < 0 || k1 > tr.steps || k0 > k1) throw std::invalid_argument("trajectory: step range out of bounds");
   if (nvec <= 0 || k0 == k1) return;
+  if (d_.model == kModelBVE3) return bve3_adj(tr, state, nvec, k0, k1, y, w);
   if (d_.model == kModelBurgers || d_.model == kModelBurgers3) {
     BurgersArgs a = burgers_args(d_);
     a.base = tr.w.get();
@@ -534,6 +604,7 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
 
 void Problem::probe_stage_kernels(const Trajectory& tr, int s, int stages, float* ms_stage, float* ms_col) const {
   if (s < 1 || stages < 1) throw std::invalid_argument("probe: need s >= 1 and stages >= 1");
+  if (d_.model == kModelBVE3) throw std::invalid_argument("probe: the stage-kernel probe covers the BASELINE models");
   cudaEvent_t ev[3];
   for (auto& e : ev) SDV_CUDA(cudaEventCreate(&e));
   wstate_.ensure(static_cast<size_t>(s) * dim_);
@@ -681,8 +752,74 @@ Problem::~Problem() {
   if (st_) cudaStreamDestroy(st_);
 }
 
+// --------------------------------------------- reference BVE (kModelBVE3) --
+void Problem::bve3_work(int nvec) const {
+  for (auto& b : b3w_) b.ensure(static_cast<size_t>(nvec) * dim_);
+}
+
+// LinearizedTrajectory::tlm_range of proj/src/bve.cpp:138-148 for a block:
+// per step d1 = d + dt J0 d, d2 = 0.75 d + 0.25 (d1 + dt J1 d1),
+// d' = d/3 + 2/3 (d2 + dt J2 d2), each J_s d needing psi' = P(d_s).
+void Problem::bve3_tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1, double* y,
+                       const double* w) const {
+  bve3_work(nvec);
+  double* st[3] = {state, b3w_[0].get(), b3w_[1].get()};
+  double* dp = b3w_[2].get();
+  for (int k = k0; k < k1; ++k) {
+    const double* wk = tr.w.get() + static_cast<long long>(k) * 3 * dim_;
+    const double* pk = tr.p.get() + static_cast<long long>(k) * 3 * dim_;
+    for (int s = 0; s < 3; ++s) {
+      poisson3_->solve(st[s], dp, nvec);
+      // stage 2 writes d' in place over d (point-wise read of d only)
+      bve3_tlm_stage(b3_, s, state, st[s], dp, wk + s * dim_, pk + s * dim_, s < 2 ? st[s + 1] : state, nvec, st_);
+      count_launch(2);  // DST scale + stage (the GEMMs are cuBLAS)
+    }
+    if (y && (k + 1) % d_.spi == 0) {
+      const int iv = (k + 1) / d_.spi - 1;
+      gather_obs(state, dim_, idx_.get(), static_cast<int>(n_obs_), w + static_cast<long long>(iv) * n_obs_,
+                 y + static_cast<long long>(iv) * n_obs_, m(), nvec, st_);
+      count_launch();
+    }
+  }
+}
+
+// adj_range of proj/src/bve.cpp:150-161 for a block: per step (reverse)
+// t2 = 2/3 (lam + dt J2^T lam), t1 = 0.25 (t2 + dt J1^T t2),
+// lam' = lam/3 + 0.75 t2 + t1 + dt J0^T t1, J^T (:199-211) with one Poisson
+// solve of its vp part; observation scatters at interval ends first.
+void Problem::bve3_adj(const Trajectory& tr, double* state, int nvec, int k0, int k1, const double* y,
+                       const double* w) const {
+  bve3_work(nvec);
+  double* t2 = b3w_[0].get();
+  double* t1 = b3w_[1].get();
+  double* vp = b3w_[2].get();
+  for (int k = k1 - 1; k >= k0; --k) {
+    if (y && (k + 1) % d_.spi == 0) {
+      const int iv = (k + 1) / d_.spi - 1;
+      scatter_obs(state, dim_, idx_.get(), static_cast<int>(n_obs_), w + static_cast<long long>(iv) * n_obs_,
+                  y + static_cast<long long>(iv) * n_obs_, m(), nvec, st_);
+      count_launch();
+    }
+    const double* wk = tr.w.get() + static_cast<long long>(k) * 3 * dim_;
+    const double* pk = tr.p.get() + static_cast<long long>(k) * 3 * dim_;
+    const double* L[3] = {t1, t2, state};  // argument of J_s^T
+    double* out[3] = {state, t1, t2};      // stage 0 writes lam' in place (point-wise read of lam only)
+    for (int s = 2; s >= 0; --s) {
+      bve3_adj_vp(b3_, L[s], wk + s * dim_, vp, nvec, st_);
+      poisson3_->solve(vp, vp, nvec);
+      bve3_adj_stage(b3_, s, L[s], vp, pk + s * dim_, state, t2, out[s], nvec, st_);
+      count_launch(3);  // vp, DST scale, stage (the GEMMs are cuBLAS)
+    }
+  }
+}
+
 void Problem::prior_inv_sqrt(const double* in, double* out, int nvec) const {
   if (d_.prior_kind != kPriorLaplacian) throw std::invalid_argument("prior_inv_sqrt: only the Laplacian prior has one");
+  if (d_.model == kModelBVE3) {
+    lap2_inv_sqrt(d_.n, d_.ny, d_.prior_alpha, d_.prior_beta, in, out, nvec, st_);
+    count_launch();
+    return;
+  }
   lap_inv_sqrt(d_.n, d_.prior_alpha, lap_b_, in, out, nvec, st_);
   count_launch();
 }

@@ -8,14 +8,16 @@
 
 #include <memory>
 
+#include "bve3_kernels.cuh"
 #include "bve_kernels.cuh"
 #include "burgers_kernels.cuh"
 #include "linalg_kernels.cuh"
 
 namespace sdv {
 
-// kModelBurgers3: the reference's own Dirichlet RK3-TVD Burgers (F3).
-enum ModelKind { kModelBurgers = 1, kModelBVE = 2, kModelBurgers3 = 3 };
+// kModelBurgers3 / kModelBVE3: the reference's own Dirichlet RK3-TVD Burgers
+// and barotropic-vorticity models (F3).
+enum ModelKind { kModelBurgers = 1, kModelBVE = 2, kModelBurgers3 = 3, kModelBVE3 = 4 };
 // kPriorFourier: B = sigma^2 C, Fourier-diagonal Gaussian (control-variable
 // background term). kPriorLaplacian: Gamma = (alpha I - beta Lap*)^{-2}
 // (proj/src/prior.cpp), x-space background term as the reference.
@@ -30,6 +32,8 @@ struct ProblemDesc {
   int block_group = 0;  // vectors per BVE sweep group (0 = auto)
   int prior_kind = kPriorFourier;
   double prior_alpha = 0, prior_beta = 0;
+  int ny = 0;                        // kModelBVE3: rows (n = nx columns)
+  double reynolds = 0, rossby = 0;   // kModelBVE3
 };
 
 class Problem;
@@ -106,6 +110,15 @@ class Problem {
   // Poisson column pass on row spectra (recurrence solver; SDV_COL_FFT=1 selects
   // the y-FFT / multiply / inverse y-FFT kernel instead).
   void poisson_col(double2* s, int nvec, cudaStream_t st) const;
+  // kModelBVE3: model constants, forcing, Poisson and prior DST solvers, and
+  // sweep workspace (5 fields per vector)
+  Bve3Args b3_;
+  DevBuf<double> forcing_;
+  std::unique_ptr<DstSolver> poisson3_, prior3_;
+  mutable DevBuf<double> b3w_[5];
+  void bve3_work(int nvec) const;
+  void bve3_tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1, double* y, const double* w) const;
+  void bve3_adj(const Trajectory& tr, double* state, int nvec, int k0, int k1, const double* y, const double* w) const;
   DevBuf<double> pivot_;  // Laplacian prior: Thomas pivots
   double lap_b_ = 0;      // beta * stencil scale
   double dt_ = 0;

@@ -32,6 +32,18 @@ def test_problem_validation_raises_invalid_argument(bad, msg):
         api.Problem(*_args(**bad))
 
 
+def test_reference_bve_validation():
+    """proj/src/bve.cpp BVEModel ctor checks (nx, ny >= 3, Re, Ro > 0) and the prior pairing."""
+    from paper_2401_15758_b200 import api
+
+    idx, vals, var = np.array([0, 5]), np.zeros((1, 2)), np.ones((1, 2))
+    base = dict(prior_kind=1, prior_alpha=0.0, prior_beta=0.06, ny=9, reynolds=200.0, rossby=0.0016)
+    args = (4, 8, 0.0, 1e-3, 1, 2, 0.0, 0.0, idx, vals, var, np.zeros(72))
+    for bad, msg in [(dict(ny=2), "BVEModel"), (dict(rossby=0.0), "BVEModel"), (dict(prior_kind=0), "Laplacian")]:
+        with pytest.raises(ValueError, match=msg):
+            api.Problem(*args, **{**base, **bad})
+
+
 @pytest.mark.parametrize("model,kind,alpha,beta,n,msg", [
     (3, 0, 0.5, 500.0, 399, "Laplacian prior"),       # Dirichlet Burgers needs the Laplacian prior
     (1, 1, 0.5, 500.0, 64, "Fourier-diagonal"),       # periodic models take the Fourier prior
