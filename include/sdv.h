@@ -144,6 +144,19 @@ int sdv_thin_qr(sdv_problem* p, int64_t n, int64_t l, const double* y, double* q
 int sdv_sketch(sdv_traj* t, int method, int rank, int rank2, uint64_t seed, double* eig, double* basis,
                int64_t counts[3]);
 
+/* adaptive_randsvd / adaptive_nystrom / adaptive_singleview
+ * (proj/src/sketch.cpp:402-564): start at rank, grow by growth while the
+ * cond_estimate probe kappa_sk > eps_sketch, capped at max_rank (rank2: the
+ * SingleView adjoint width cap, <= 0 for 2 max_rank + 1). eig/basis sized
+ * for max_rank; counts = {tlm, adj, final_rank, probes, tolerance_met};
+ * kappa (may be NULL) receives the kappa_sk history, up to max_kappa values. */
+int sdv_sketch_adaptive(sdv_traj* t, int method, int rank, int growth, int max_rank, int rank2, double eps_sketch,
+                        uint64_t seed, double* eig, double* basis, int64_t counts[5], double* kappa, int max_kappa);
+
+/* cond_estimate (proj/src/sketch.cpp:391-400): kappa of (I + H)(I + H_hat)^{-1}
+ * from one seeded probe, H_hat = (basis, eig) of rank l. */
+int sdv_cond_estimate(sdv_traj* t, int64_t l, const double* basis, const double* eig, uint64_t seed, double* kappa);
+
 /* pcg_solve (proj/src/linalg.cpp:52-106) on (I + H) x = rhs at trajectory t,
  * preconditioned by woodbury_apply with (basis, eig) when l > 0.
  * info = {iterations, converged}. */

@@ -209,6 +209,55 @@ int oracle_sketch(int h, int t, int method, int rank, int rank2, uint64_t seed, 
     counts[2] = r.final_rank;
   });
 }
+// Adaptive sketches (offline map a / h, online probe map h), as gn_solve wires
+// them. counts: [tlm, adj, final_rank, probe_applies, tolerance_met].
+int oracle_sketch_adaptive(int h, int t, int method, int rank, int growth, int max_rank, int rank2, double eps,
+                           uint64_t seed, int workers, double* eig, double* basis, int64_t* counts, double* kappa,
+                           int max_kappa) {
+  return guard([&] {
+    const auto& p = sc(h).problem;
+    const MisfitOperator op(p, tr(t));
+    const GramMap hoff(op), hon(op);
+    SketchConfig c;
+    c.method = meth(method);
+    c.rank = rank;
+    c.growth = growth;
+    c.max_rank = max_rank;
+    c.rank2 = rank2;
+    c.eps_sketch = eps;
+    c.seed = seed;
+    c.workers = workers;
+    SketchReport r;
+    switch (c.method) {
+      case SketchMethod::RandSVD: r = adaptive_randsvd(op, c, hon); break;
+      case SketchMethod::Nystrom: r = adaptive_nystrom(hoff, c, &hon); break;
+      case SketchMethod::SingleView: r = adaptive_singleview(op, c, hon); break;
+      default: throw std::invalid_argument("oracle_sketch_adaptive: method must be 0, 1 or 2");
+    }
+    vout(r.evd.eigenvalues, eig);
+    if (basis) vout(r.evd.basis.a, basis);
+    counts[0] = r.tlm_applies;
+    counts[1] = r.adj_applies;
+    counts[2] = r.final_rank;
+    counts[3] = r.probe_applies;
+    counts[4] = r.tolerance_met;
+    if (kappa)
+      for (int i = 0; i < max_kappa && i < static_cast<int>(r.kappa_history.size()); ++i) kappa[i] = r.kappa_history[i];
+  });
+}
+int oracle_cond_estimate(int h, int t, int64_t l, const double* basis, const double* eig, uint64_t seed,
+                         double* kappa) {
+  return guard([&] {
+    const auto& p = sc(h).problem;
+    const MisfitOperator op(p, tr(t));
+    const GramMap hop(op);
+    LowRankEVD e;
+    e.basis = Mat(p.state_dim(), l);
+    e.basis.a.assign(basis, basis + p.state_dim() * l);
+    e.eigenvalues.assign(eig, eig + l);
+    *kappa = cond_estimate(hop, e, seed);
+  });
+}
 // GN solve. params: [mode, method, rank, rank2, growth, max_rank, max_gn_iters, pcg_max_iter, workers]
 // dparams: [grad_tol, pcg_tol, eps_sketch, eps_reuse]; negative/zero entries keep scenario defaults.
 // log: per iteration 16 doubles: k, cost, gnorm, step, pcg_iters, ls_trials, pcg_conv, recomputed,

@@ -83,6 +83,9 @@ def lib():
         "sdv_thin_qr": (C.c_int, [vp, C.c_int64, C.c_int64, D, D, D, I32]),
         "sdv_sketch": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_uint64, D, D, I64]),
         "sdv_pcg_solve": (C.c_int, [vp, D, C.c_int64, D, D, C.c_double, C.c_int, D, I32]),
+        "sdv_sketch_adaptive": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64,
+                                          D, D, I64, D, C.c_int]),
+        "sdv_cond_estimate": (C.c_int, [vp, C.c_int64, D, D, C.c_uint64, D]),
         "sdv_gn_solve": (C.c_int, [vp, C.POINTER(GNConfigC), D, D, C.c_int, I32, D, D, C.c_int]),
         "sdv_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
         "sdv_gaussian_matrix": (C.c_int, [C.c_int64, C.c_int64, C.c_uint64, D]),

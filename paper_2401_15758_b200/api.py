@@ -250,6 +250,26 @@ class Trajectory:
         k = int(counts[2])
         return eig[:k], (basis[:k] if basis is not None else None), counts
 
+    def sketch_adaptive(self, method, rank, growth, max_rank, seed, rank2=-1, eps_sketch=1.5):
+        """adaptive_{randsvd,nystrom,singleview} (proj/src/sketch.cpp:402-564).
+
+        Returns (eig, basis, counts = [tlm, adj, final_rank, probes, tolerance_met], kappa history)."""
+        eig = np.empty(max_rank)
+        basis = np.empty((max_rank, self.problem.n))
+        counts = np.zeros(5, np.int64)
+        kappa = np.full(64, np.nan)
+        check(lib().sdv_sketch_adaptive(self._h, method, rank, growth, max_rank, rank2, eps_sketch, seed, _p(eig),
+                                        _p(basis), counts.ctypes.data_as(I64), _p(kappa), kappa.size))
+        k = int(counts[2])
+        return eig[:k], basis[:k], counts, kappa[~np.isnan(kappa)]
+
+    def cond_estimate(self, basis, eig, seed):
+        """cond_estimate (proj/src/sketch.cpp:391-400) of (I + H)(I + H_hat)^-1."""
+        basis = _f64(np.atleast_2d(basis))
+        out = C.c_double()
+        check(lib().sdv_cond_estimate(self._h, basis.shape[0], _p(basis), _p(_f64(eig)), seed, C.byref(out)))
+        return out.value
+
     def pcg_solve(self, rhs, basis=None, eig=None, tol=1e-9, max_iter=10000):
         l = 0 if basis is None else np.atleast_2d(basis).shape[0]
         x = np.empty(self.problem.n)

@@ -312,6 +312,53 @@ int sdv_sketch(sdv_traj* t, int method, int rank, int rank2, uint64_t seed, doub
   });
 }
 
+int sdv_sketch_adaptive(sdv_traj* t, int method, int rank, int growth, int max_rank, int rank2, double eps_sketch,
+                        uint64_t seed, double* eig, double* basis, int64_t counts[5], double* kappa, int max_kappa) {
+  return guard([&] {
+    need(t, "trajectory");
+    need(eig, "eig");
+    need(counts, "counts");
+    if (method < 0 || method > 2) throw std::invalid_argument("sdv_sketch_adaptive: method must be 0, 1 or 2");
+    auto& q = *t->owner->p;
+    sdv::SketchCfg c;
+    c.method = method;
+    c.rank = rank;
+    c.growth = growth;
+    c.max_rank = max_rank;
+    c.rank2 = rank2;
+    c.eps_sketch = eps_sketch;
+    c.seed = seed;
+    // offline (sketch) and online (probe) applications are charged separately,
+    // as gn_solve does (proj/src/fourdvar.cpp:257-324)
+    sdv::MisfitOp off(q, *t->t), on(q, *t->t);
+    sdv::SketchResult r = method == 0   ? sdv::adaptive_randsvd(off, c, on)
+                          : method == 1 ? sdv::adaptive_nystrom(off, c, on)
+                                        : sdv::adaptive_singleview(off, c, on);
+    std::memcpy(eig, r.evd.eig.data(), sizeof(double) * r.evd.l);
+    if (basis) r.evd.basis.download(basis, static_cast<size_t>(q.dim()) * r.evd.l, q.stream());
+    SDV_CUDA(cudaStreamSynchronize(q.stream()));
+    counts[0] = r.tlm;
+    counts[1] = r.adj;
+    counts[2] = r.final_rank;
+    counts[3] = r.probes;
+    counts[4] = r.tolerance_met;
+    if (kappa)
+      for (int i = 0; i < max_kappa && i < static_cast<int>(r.kappa.size()); ++i) kappa[i] = r.kappa[i];
+  });
+}
+
+int sdv_cond_estimate(sdv_traj* t, int64_t l, const double* basis, const double* eig, uint64_t seed, double* kappa) {
+  return guard([&] {
+    need(t, "trajectory");
+    need(kappa, "kappa");
+    auto& q = *t->owner->p;
+    sdv::DeviceEVD e;
+    if (l > 0) e.upload(q.dim(), static_cast<int>(l), basis, eig, q.stream());
+    sdv::MisfitOp op(q, *t->t);
+    *kappa = sdv::cond_estimate(op, e, seed);
+  });
+}
+
 int sdv_pcg_solve(sdv_traj* t, const double* rhs, int64_t l, const double* basis, const double* eig, double tol,
                   int max_iter, double* x, int info[2]) {
   return guard([&] {

@@ -38,6 +38,9 @@ def lib():
         _lib.oracle_gn_solve.argtypes = [C.c_int, I64, D, C.c_uint64, D, D, C.c_int, C.POINTER(C.c_int), D, D,
                                          C.c_int]
         _lib.oracle_sketch.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, D, D, I64]
+        _lib.oracle_sketch_adaptive.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                                C.c_double, C.c_uint64, C.c_int, D, D, I64, D, C.c_int]
+        _lib.oracle_cond_estimate.argtypes = [C.c_int, C.c_int, C.c_int64, D, D, C.c_uint64, D]
         _lib.oracle_sketch_dense.argtypes = [C.c_int64, C.c_int64, D, C.c_int, C.c_int, C.c_int, C.c_uint64, D, D]
         _lib.oracle_bve_fixture.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
                                             C.c_uint64, D]
@@ -178,6 +181,23 @@ class Trajectory:
         _chk(lib().oracle_sketch(self.sc.h, self.h, method, rank, rank2, seed, workers, _p(eig), _p(basis),
                                  counts.ctypes.data_as(I64)))
         return eig, basis, counts
+
+    def sketch_adaptive(self, method, rank, growth, max_rank, seed, rank2=-1, eps=1.5, workers=1):
+        eig = np.empty(max_rank)
+        basis = np.empty((max_rank, self.sc.n))
+        counts = np.zeros(5, np.int64)
+        kappa = np.full(64, np.nan)
+        _chk(lib().oracle_sketch_adaptive(self.sc.h, self.h, method, rank, growth, max_rank, rank2, eps, seed,
+                                          workers, _p(eig), _p(basis), counts.ctypes.data_as(I64), _p(kappa), 64))
+        k = int(counts[2])
+        return eig[:k], basis[:k], counts, kappa[~np.isnan(kappa)]
+
+    def cond_estimate(self, basis, eig, seed):
+        basis = np.ascontiguousarray(np.atleast_2d(basis), np.float64)
+        out = C.c_double()
+        _chk(lib().oracle_cond_estimate(self.sc.h, self.h, basis.shape[0], _p(basis),
+                                        _p(np.ascontiguousarray(eig, np.float64)), seed, C.byref(out)))
+        return out.value
 
     def __del__(self):
         try:

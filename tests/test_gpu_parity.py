@@ -187,3 +187,20 @@ def test_gn_solve_parity(oracle, sdv, cfg, mode, method, steps, iters):
     assert np.array_equal(rg["log"][:, 14:16], ro["log"][:, 14:16])
     if len(ro["eig0"]):
         assert eig_rel(rg["eig0"], ro["eig0"]) <= 1e-8
+
+
+@pytest.mark.parametrize("cfg,steps,method", [(0, -1, 0), (0, -1, 1), (0, -1, 2), (2, 20, 1), (2, 20, 2)])
+def test_adaptive_sketch_and_cond_estimate_parity(oracle, sdv, cfg, steps, method):
+    """adaptive_{randsvd,nystrom,singleview} + cond_estimate (proj/src/sketch.cpp:391-564): the same
+    growth decisions (final rank, applies, probes), kappa history and eigenvalues as the oracle."""
+    osc, prob = pair(oracle, cfg, steps=steps)
+    otr = osc.linearize(osc.background)
+    gtr = prob.linearize(osc.background)
+    eo, bo, co, ko = otr.sketch_adaptive(method, 5, 5, 40, 123, workers=8)
+    eg, bg, cg, kg = gtr.sketch_adaptive(method, 5, 5, 40, 123)
+    assert tuple(cg) == tuple(co)
+    assert len(kg) == len(ko) and np.allclose(kg, ko, rtol=1e-8, atol=0)
+    assert eig_rel(eg, eo) <= 1e-8
+    ko1 = otr.cond_estimate(bo, eo, 9)
+    kg1 = gtr.cond_estimate(bg, eg, 9)
+    assert abs(kg1 - ko1) <= 1e-8 * abs(ko1)
