@@ -45,7 +45,9 @@ def parse():
     ap.add_argument("--sweep", default="", help="extra block widths to report, e.g. 1,8,32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--gn", default="", help="also time full GN solves for these configs, e.g. 0,1,2,4 (or 'all')")
+    ap.add_argument("--gn", default="auto",
+                    help="also time full GN solves (the metric's second half) for these configs, e.g. 0,1,2,4, "
+                         "'all', or 'none'; 'auto' = 0,1,2 at N=1 (C3/C4 take 1-3 min each), none under torchrun")
     ap.add_argument("--window", type=int, default=0,
                     help="profiling only (ncu launch lists): shorten the model window to this many RK4 steps "
                          "(2 observation intervals); the reported line then names the window in config")
@@ -404,8 +406,11 @@ def run_ours(args, world, rank, local):
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches}
         if sweep:
             line["block_sweep"] = sweep
-        if args.gn:
-            cfgs = [0, 1, 2, 3, 4] if args.gn == "all" else [int(x) for x in args.gn.split(",") if x]
+        gn = args.gn
+        if gn == "auto":
+            gn = "0,1,2" if world == 1 and not args.window else "none"
+        if gn and gn != "none":
+            cfgs = [0, 1, 2, 3, 4] if gn == "all" else [int(x) for x in gn.split(",") if x]
             line["gn_solve"] = [gn_solve_timing(c) for c in cfgs]
         print(json.dumps(line), flush=True)
     if dist is not None:
