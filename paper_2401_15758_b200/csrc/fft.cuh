@@ -221,51 +221,6 @@ __device__ __forceinline__ void fft_team(double2* buf, const double2* __restrict
   }
 }
 
-// Warp-private variant: one length-N transform per warp, each lane playing
-// VT = N/256 "virtual" team threads (t = lane + 32 j), so a lane carries
-// 8 VT values per pass (independent butterflies: ILP) and the passes exchange
-// through the warp's own padded buffer with __syncwarp only — no CTA-wide
-// barriers, so warps drift and hide each other's latency. N >= 256.
-template <int N, bool INV, int PASS = 0, class Load, class Store>
-__device__ __forceinline__ void fft_warp(double2* buf, const double2* __restrict__ tw, int lane, Load& load,
-                                         Store& store) {
-  using P = FftPass<N, PASS>;
-  constexpr int R = P::R, G = 8 / R, VT = N / 256;
-  static_assert(N >= 256, "fft_warp needs N >= 256");
-  double2 v[VT][8];
-#pragma unroll
-  for (int j = 0; j < VT; ++j) {
-    const int t = lane + 32 * j;
-#pragma unroll
-    for (int q = 0; q < G; ++q)
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = fft_in_index<N, PASS>(t, q, r);
-        if constexpr (PASS == 0) v[j][q * R + r] = load(i);
-        else v[j][q * R + r] = buf[fpad(i)];
-      }
-  }
-#pragma unroll
-  for (int j = 0; j < VT; ++j) fft_pass_compute<N, PASS, INV>(v[j], lane + 32 * j, tw);
-  __syncwarp();  // every read of buf in this pass precedes the in-place writes
-  if constexpr (P::LAST) {
-#pragma unroll
-    for (int j = 0; j < VT; ++j)
-#pragma unroll
-      for (int q = 0; q < G; ++q)
-#pragma unroll
-        for (int r = 0; r < R; ++r) store(fft_out_index<N, PASS>(lane + 32 * j, q, r), v[j][q * R + r]);
-  } else {
-#pragma unroll
-    for (int j = 0; j < VT; ++j)
-#pragma unroll
-      for (int q = 0; q < G; ++q)
-#pragma unroll
-        for (int r = 0; r < R; ++r) buf[fpad(fft_out_index<N, PASS>(lane + 32 * j, q, r))] = v[j][q * R + r];
-    __syncwarp();
-    fft_warp<N, INV, PASS + 1>(buf, tw, lane, load, store);
-  }
-}
 #endif
 
 // Device twiddle table exp(-2 pi i m / N), m in [0, N); cached per length.
