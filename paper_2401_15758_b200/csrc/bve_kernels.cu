@@ -18,6 +18,7 @@
 //                 Arakawa/Laplacian stencils with the stored base stage fields,
 //                 the RK4 (TLM/NL) or adjoint-RK4 (ADJ) update, and the forward
 //                 x-FFT of the next stage's Poisson input for the owned rows.
+#include <cstdlib>
 #include <type_traits>
 
 #include "bve_kernels.cuh"
@@ -340,9 +341,221 @@ __global__ void __launch_bounds__(256, N >= 512 ? 2 : 3)
   }
 }
 
+// ----------------------------------------------- tile carries (fused path) --
+// Packed kx = 0 column of one vector, one warp, exact O(N) solves (lane l owns
+// rows l*RPS .. l*RPS + RPS - 1):
+//  * real part, x-mode 0: the zero-mean pseudo-inverse of the periodic second
+//    difference L = 2 - S - S^-1 (the (0,0) mode of psi is 0): with
+//    w' = w - mean(w), P_j = sum_{m<j} w'_m, S_j = sum_{i=1}^{j} P_i,
+//    D_0 = S_N / N, psi_j = j D_0 - S_j minus its mean;
+//  * imaginary part, x-mode N/2: (6 - S - S^-1)^-1 by the cyclic forward and
+//    backward recurrences with rho = 3 - 2 sqrt 2, as col_solve_kernel.
+// Both times h^2 / N (the 1/N is the unnormalised inverse x-FFT): the same
+// operator as the spectral column pass (mu = 4 sin^2(pi ky / N) / h^2).
+// t0 = tab[0] = {rho_{N/2}, h^2 / N, 1 / (1 - rho_{N/2}^N), h^2 rho_{N/2} / N}.
+template <int N>
+__device__ __forceinline__ void col0_warp_solve(double2* __restrict__ col, double4 t0, int lane) {
+  constexpr unsigned kAll = 0xffffffffu;
+  constexpr int RPS = N / 32;
+  double2 x[RPS];
+#pragma unroll
+  for (int k = 0; k < RPS; ++k) x[k] = col[static_cast<long long>(lane * RPS + k) * (N / 2)];
+  auto warp_sum = [&](double a) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) a += __shfl_xor_sync(kAll, a, d);
+    return a;
+  };
+  auto warp_excl = [&](double a) {  // exclusive prefix sum over lanes
+    double incl = a;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double o = __shfl_up_sync(kAll, incl, d);
+      if (lane >= d) incl += o;
+    }
+    return incl - a;
+  };
+  // ---- real part (singular) ----
+  double ls = 0.0;
+#pragma unroll
+  for (int k = 0; k < RPS; ++k) ls += x[k].x;
+  const double mean = warp_sum(ls) / N;
+  double pre[RPS];  // P_j at row j = lane*RPS + k (exclusive prefix of w')
+  {
+    double run = warp_excl(ls - RPS * mean);
+#pragma unroll
+    for (int k = 0; k < RPS; ++k) {
+      pre[k] = run;
+      run += x[k].x - mean;
+    }
+  }
+  // S_j = sum_{i=1}^{j} P_i (P_0 = 0, so S_j = inclusive prefix of P)
+  double lp = 0.0;
+#pragma unroll
+  for (int k = 0; k < RPS; ++k) lp += pre[k];
+  const double d0 = warp_sum(lp) / N;  // S_N / N (P_N = 0)
+  double ps = 0.0;
+  {
+    double run = warp_excl(lp);
+#pragma unroll
+    for (int k = 0; k < RPS; ++k) {
+      run += pre[k];
+      pre[k] = static_cast<double>(lane * RPS + k) * d0 - run;  // psi_j before centring
+      ps += pre[k];
+    }
+  }
+  const double pm = warp_sum(ps) / N;
+  // ---- imaginary part (x-mode N/2) ----
+  const double rho = t0.x;
+  double2 slot;
+  double f = 0.0;
+#pragma unroll
+  for (int k = 0; k < RPS; ++k) {
+    f = fma(rho, f, x[k].y);
+    x[k].y = f;
+  }
+  double rR = 1.0;
+#pragma unroll
+  for (int k = 0; k < RPS; ++k) rR *= rho;
+  slot = make_double2(f, 0.0);
+  carry_scan<true>(slot, rR, t0.z, lane);
+  {
+    double pw = rho;
+#pragma unroll
+    for (int k = 0; k < RPS; ++k) {
+      x[k].y = fma(pw, slot.x, x[k].y);
+      pw *= rho;
+    }
+  }
+  double g = 0.0;
+#pragma unroll
+  for (int k = RPS - 1; k >= 0; --k) {
+    g = fma(rho, g, x[k].y);
+    x[k].y = g;
+  }
+  slot = make_double2(g, 0.0);
+  carry_scan<false>(slot, rR, t0.z, lane);
+  double pw = rho;
+#pragma unroll
+  for (int k = RPS - 1; k >= 0; --k) {
+    x[k].y = t0.w * fma(pw, slot.x, x[k].y);
+    pw *= rho;
+  }
+#pragma unroll
+  for (int k = 0; k < RPS; ++k)
+    col[static_cast<long long>(lane * RPS + k) * (N / 2)] = make_double2(t0.y * (pre[k] - pm), x[k].y);
+}
+
+// Tile carries per x-mode kx >= 1 (32 adjacent modes per CTA, lane = mode;
+// warp = part of QP = Q/8 consecutive 8-row tiles): the forward carries C_q
+// (F at the last row of tile q-1) from the tile end values L_q,
+// C_{q+1} = L_q + rho^8 C_q, and the backward carries E_q (G at the first row
+// of tile q+1) from V_q = M_q + alpha_0 C_q + rho^8 V_{q+1}, M_q = H at the
+// first row of tile q, both cyclic (closure 1/(1 - rho^N)). The 8 part maps
+// are composed through shared memory. The grid's last CTA column solves the
+// packed kx = 0 column in place (col0_warp_solve).
+template <int N>
+__global__ void __launch_bounds__(256, 2) carry_kernel(double2* __restrict__ s, const double2* __restrict__ lsum,
+                                                    double2* __restrict__ car_c, double2* __restrict__ car_e,
+                                                    const double4* __restrict__ tab) {
+  constexpr int T = 8, Q = N / T, NPT = 8, QP = Q / NPT;
+  static_assert(Q % NPT == 0, "carry_kernel: N / 8 tiles must split into 8 parts");
+  pdl_trigger();
+  pdl_wait();
+  const int lane = threadIdx.x % 32, pt = threadIdx.x / 32;
+  const long long v = blockIdx.y;
+  if (blockIdx.x == gridDim.x - 1) {
+    if (pt == 0) col0_warp_solve<N>(s + v * N * (N / 2), tab[0], lane);
+    return;
+  }
+  __shared__ double2 part[NPT][32];
+  const int kx = blockIdx.x * 32 + lane;
+  const bool live = kx != 0 && kx < N / 2;
+  const int kxs = live ? kx : 1;
+  const double4 tb = tab[kxs];
+  const long long cb = v * Q * (N / 2) + kxs;
+  double2 Lv[QP], Mv[QP];
+#pragma unroll
+  for (int i = 0; i < QP; ++i) {
+    const int q = pt * QP + i;
+    Lv[i] = lsum[cb + static_cast<long long>(q) * (N / 2)];
+    Mv[i] = s[v * N * (N / 2) + static_cast<long long>(q) * T * (N / 2) + kxs];
+  }
+  const double rho = tb.x, clos = tb.z;
+  double rT = rho * rho;
+  rT *= rT;
+  rT *= rT;  // rho^8
+  double A = 1.0;  // part map multiplier rho^(8 QP)
+#pragma unroll
+  for (int i = 0; i < QP; ++i) A *= rT;
+  double a0 = 0.0;  // alpha_0 = sum_{m<8} rho^(2m+1)
+  {
+    double pw = rho;
+#pragma unroll
+    for (int m = 0; m < T; ++m) {
+      a0 += pw;
+      pw *= rho * rho;
+    }
+  }
+  // forward: part composition with zero carry-in, then the closed carry
+  double2 f = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < QP; ++i) f = make_double2(fma(rT, f.x, Lv[i].x), fma(rT, f.y, Lv[i].y));
+  part[pt][lane] = f;
+  __syncthreads();
+  double2 tot = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int p = 0; p < NPT; ++p) {
+    const double2 fp = part[p][lane];
+    tot = make_double2(fma(A, tot.x, fp.x), fma(A, tot.y, fp.y));
+  }
+  double2 cin = make_double2(clos * tot.x, clos * tot.y);  // C_0
+  for (int p = 0; p < pt; ++p) {
+    const double2 fp = part[p][lane];
+    cin = make_double2(fma(A, cin.x, fp.x), fma(A, cin.y, fp.y));
+  }
+#pragma unroll
+  for (int i = 0; i < QP; ++i) {
+    if (live) car_c[cb + static_cast<long long>(pt * QP + i) * (N / 2)] = cin;
+    Mv[i] = make_double2(fma(a0, cin.x, Mv[i].x), fma(a0, cin.y, Mv[i].y));  // u_q
+    cin = make_double2(fma(rT, cin.x, Lv[i].x), fma(rT, cin.y, Lv[i].y));
+  }
+  // backward: V at the first tile of each part with zero carry from above
+  double2 g = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int i = QP - 1; i >= 0; --i) g = make_double2(fma(rT, g.x, Mv[i].x), fma(rT, g.y, Mv[i].y));
+  __syncthreads();
+  part[pt][lane] = g;
+  __syncthreads();
+  double2 vt = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int p = NPT - 1; p >= 0; --p) {
+    const double2 gp = part[p][lane];
+    vt = make_double2(fma(A, vt.x, gp.x), fma(A, vt.y, gp.y));
+  }
+  double2 e = make_double2(clos * vt.x, clos * vt.y);  // V at tile 0 (= part NPT, cyclic)
+  for (int p = NPT - 1; p > pt; --p) {
+    const double2 gp = part[p][lane];
+    e = make_double2(fma(A, e.x, gp.x), fma(A, e.y, gp.y));
+  }
+  if (!live) return;
+#pragma unroll
+  for (int i = QP - 1; i >= 0; --i) {
+    const long long o = cb + static_cast<long long>(pt * QP + i) * (N / 2);
+    car_e[o] = e;
+    e = make_double2(fma(rT, e.x, Mv[i].x), fma(rT, e.y, Mv[i].y));
+  }
+}
+
 // --------------------------------------------------------- fused RK stage --
 // ST: RK stage as a compile-time constant (TLM/ADJ; -1 = runtime p.stage).
-template <int N, int MODE, int T, int ST = -1>
+// FUS: fused Poisson path (TLM/ADJ, T = 8). The launch stages its spectrum
+// rows and stencil-input rows into shared memory with cp.async up front,
+// reconstructs the y-solved spectra from the tile-local recurrence values
+// and the tile carries of bve_carry, runs both x-FFTs in place in P (swizzled
+// layout, no scratch buffer), and ends with the tile-local forward/backward
+// recurrences of the next Poisson solve on its own rows, so the full-field
+// column pass (read + write of every spectrum) drops out of each stage.
+template <int N, int MODE, int T, int ST = -1, bool FUS = false>
 __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
   using C = Cfg<N, T>;
   constexpr int R = T + 2;
@@ -370,12 +583,12 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
   if (pf) {
     if (MODE == kModeTlm) {
       prefetch_rows<N, true>(p.base_p, y0 - 1, R, tid, kThreads);
-      prefetch_rows<N, false>(p.x_in + off, y0 - 1, R, tid, kThreads);
+      if (!FUS) prefetch_rows<N, false>(p.x_in + off, y0 - 1, R, tid, kThreads);
       if (stage >= 1 && stage <= 2) prefetch_rows<N, false>(p.d + off, y0, T, tid, kThreads);
       if (stage >= 1) prefetch_rows<N, false>(p.acc + off, y0, T, tid, kThreads);
     } else if (MODE == kModeAdj && !finish) {
       prefetch_rows<N, true>(p.base_p, y0 - 1, R, tid, kThreads);
-      if (has_prev) prefetch_rows<N, false>(p.q_in + off, y0 - 1, R, tid, kThreads);
+      if (has_prev && !FUS) prefetch_rows<N, false>(p.q_in + off, y0 - 1, R, tid, kThreads);
       prefetch_rows<N, false>(p.acc + off, y0 - 1, R, tid, kThreads);
       prefetch_rows<N, false>(p.d + off, y0 - 1, R, tid, kThreads);
     }
@@ -383,8 +596,86 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
 
   pdl_wait();  // everything below reads what the previous launch wrote
 
+  if constexpr (FUS) {
+    // Phase 0: every global tile read of the launch in flight at once. The
+    // stencil input (TLM x_in, ADJ q_in) streams into X by cp.async; the
+    // spectrum rows y0-1 .. y0+T go through registers into P (a packed
+    // spectrum row is N doubles, the size of a field row): thread kx loads its
+    // column of the R rows plus the carries of the three tiles involved and
+    // stores the y-solved values psi = scale (H + alpha_o C_q + rho^(T-o) E_q)
+    // (row offset o of tile q, alpha_o = sum_{m=o}^{T-1} rho^(2m-o+1), see
+    // bve_carry). kx = 0 and first-stage (kFlagRawIn) spectra are final.
+    const bool inv = has_prev && !(p.flags & kFlagSkipInvFft);
+    const double* xsrc = MODE == kModeTlm ? p.x_in : (has_prev ? p.q_in : nullptr);
+    if (xsrc) {
+      xsrc += off;
+      for (int e = 2 * tid; e < R * N; e += 2 * kThreads) {
+        const int r = e / N, x = e % N;
+        cp_async16(X + e, xsrc + static_cast<long long>((y0 - 1 + r) & (N - 1)) * N + x);
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    if (inv) {
+      constexpr int Q = N / T;
+      const bool raw = p.flags & kFlagRawIn;
+      const int q0 = blockIdx.x, qm = (q0 + Q - 1) % Q, qp = (q0 + 1) % Q;
+      for (int kx = tid; kx < N / 2; kx += kThreads) {
+        const double2* hs = p.s_in + soff + kx;
+        double2 h[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) h[r] = hs[static_cast<long long>((y0 - 1 + r) & (N - 1)) * (N / 2)];
+        if (kx != 0 && !raw) {
+          const long long cb = static_cast<long long>(v) * Q * (N / 2) + kx;
+          const double2 cm = p.car_c[cb + qm * (N / 2)], c0 = p.car_c[cb + q0 * (N / 2)],
+                        cq = p.car_c[cb + qp * (N / 2)];
+          const double2 em = p.car_e[cb + qm * (N / 2)], e0 = p.car_e[cb + q0 * (N / 2)],
+                        eq = p.car_e[cb + qp * (N / 2)];
+          const double4 tb = p.stab[kx];
+          const double rho = tb.x, scale = tb.w;
+          double pw[T + 1], al[T];
+          pw[0] = 1.0;
+#pragma unroll
+          for (int i = 1; i <= T; ++i) pw[i] = pw[i - 1] * rho;
+          al[T - 1] = pw[T];
+#pragma unroll
+          for (int o = T - 2; o >= 0; --o) al[o] = fma(rho, al[o + 1], pw[o + 1]);
+          auto fix = [&](double2& z, double a, double b, double2 c, double2 e) {
+            z = make_double2(scale * fma(b, e.x, fma(a, c.x, z.x)), scale * fma(b, e.y, fma(a, c.y, z.y)));
+          };
+          fix(h[0], al[T - 1], pw[1], cm, em);
+#pragma unroll
+          for (int o = 0; o < T; ++o) fix(h[1 + o], al[o], pw[T - o], c0, e0);
+          fix(h[R - 1], al[0], pw[T], cq, eq);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) reinterpret_cast<double2*>(P + r * N)[kx] = h[r];
+      }
+    }
+    if (xsrc) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    if (inv) {
+      // Phase 1: inverse x-FFT of the R rows, in place (pair region of P).
+      constexpr int kPairs = R / 2;
+#pragma unroll 1
+      for (int b0 = 0; b0 < kPairs; b0 += C::kTeams) {
+        const int pr = b0 + team;
+        const bool act = pr < kPairs;
+        double* pa = P + (2 * pr) * N;
+        double2* buf = reinterpret_cast<double2*>(pa);
+        const double2* ra = buf;
+        const double2* rb = buf + N / 2;
+        auto load = [&](int i) { return unpack_elem<N>(ra, rb, i); };
+        auto store = [&](int i, double2 z) {
+          pa[i] = z.x;
+          pa[i + N] = z.y;
+        };
+        fft_team<N, true, 0, true>(buf, tw, t, act, load, store);
+        __syncthreads();
+      }
+    }
+  }
   // Phase 1: inverse x-FFT of rows y0-1 .. y0+T -> P.
-  if (has_prev && !(p.flags & kFlagSkipInvFft)) {
+  if (!FUS && has_prev && !(p.flags & kFlagSkipInvFft)) {
     constexpr int kPairs = R / 2;
 #pragma unroll 1
     for (int b0 = 0; b0 < kPairs; b0 += C::kTeams) {
@@ -405,7 +696,9 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
   }
 
   // Phase 2: stencil-input rows (overwrite the FFT buffers).
-  if (MODE != kModeAdj) {
+  if (FUS && MODE == kModeTlm) {
+    // staged in phase 0
+  } else if (MODE != kModeAdj) {
     const double* xin = p.x_in + off;
     for (int e = 2 * tid; e < R * N; e += 2 * kThreads) {
       const int r = e / N, x = e % N;
@@ -437,7 +730,8 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
         for (int u = 0; u < kRB; ++u) {
           const int r = rb + u;
           go[u] = (off + static_cast<long long>((y0 - 1 + r) & (N - 1)) * N) / 2 + x2;
-          qv[u] = has_prev ? qin[go[u]] : z2;
+          if (FUS) qv[u] = has_prev ? reinterpret_cast<const double2*>(X + r * N)[x2] : z2;  // staged
+          else qv[u] = has_prev ? qin[go[u]] : z2;
           av[u] = need_a ? accp[go[u]] : z2;
           lv[u] = need_l ? lamp[go[u]] : z2;
         }
@@ -701,6 +995,64 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
 
   // Phase 4: forward x-FFT of the owned rows -> next row spectra.
   constexpr int kOwnPairs = T / 2;
+  if constexpr (FUS) {
+    if (p.flags & kFlagSkipFwdFft) return;
+    // in place per pair region (rows 1+2pr, 2+2pr of P); T = 8 rows are one
+    // round (kTeams >= 4 for every N <= 512)
+    static_assert(kOwnPairs <= C::kTeams, "fused path: one forward FFT round");
+    {
+      const int pr = team;
+      const bool act = pr < kOwnPairs;
+      const double* pa = P + (1 + 2 * pr) * N;
+      double2* buf = reinterpret_cast<double2*>(P + (1 + 2 * pr) * N);
+      auto load = [&](int i) { return make_double2(pa[i], pa[i + N]); };
+      auto store = [&](int i, double2 z) { buf[fswz(i)] = z; };
+      fft_team<N, false, 0, true>(buf, tw, t, act, load, store);
+      __syncthreads();
+    }
+    // Tile-local y-recurrences of the next Poisson solve, per x-mode kx
+    // (thread kx unpacks the two real rows of each pair from Z(kx), Z(N-kx)):
+    // F_o = w_o + rho F_{o-1} (F_{-1} = 0), L = F_{T-1};
+    // H_o = F_o + rho H_{o+1} (H_T = 0). Column kx = 0 is stored raw
+    // (packed X(0) + i X(N/2)).
+    constexpr int Q = N / T;
+    for (int kx = tid; kx < N / 2; kx += kThreads) {
+      double2 w[T];
+#pragma unroll
+      for (int pr = 0; pr < kOwnPairs; ++pr) {
+        const double2* z = reinterpret_cast<const double2*>(P + (1 + 2 * pr) * N);
+        if (kx == 0) {
+          const double2 z0 = z[0], zn = z[fswz(N / 2)];
+          w[2 * pr] = make_double2(z0.x, zn.x);
+          w[2 * pr + 1] = make_double2(z0.y, zn.y);
+        } else {
+          const double2 zk = z[fswz(kx)], zm = z[fswz(N - kx)];
+          w[2 * pr] = make_double2(0.5 * (zk.x + zm.x), 0.5 * (zk.y - zm.y));
+          w[2 * pr + 1] = make_double2(0.5 * (zk.y + zm.y), -0.5 * (zk.x - zm.x));
+        }
+      }
+      double2* out = p.s_out + soff + static_cast<long long>(y0) * (N / 2) + kx;
+      if (kx != 0) {
+        const double rho = p.stab[kx].x;
+        double2 f = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int o = 0; o < T; ++o) {
+          f = make_double2(fma(rho, f.x, w[o].x), fma(rho, f.y, w[o].y));
+          w[o] = f;
+        }
+        p.lsum[(v * Q + blockIdx.x) * (N / 2) + kx] = f;
+        double2 g = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int o = T - 1; o >= 0; --o) {
+          g = make_double2(fma(rho, g.x, w[o].x), fma(rho, g.y, w[o].y));
+          w[o] = g;
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < T; ++o) out[static_cast<long long>(o) * (N / 2)] = w[o];
+    }
+    return;
+  }
 #pragma unroll 1
   for (int b0 = 0; b0 < ((p.flags & kFlagSkipFwdFft) ? 0 : kOwnPairs); b0 += C::kTeams) {
     const int pr = b0 + team;
@@ -762,6 +1114,7 @@ struct Launch {
     if (done) return;
     stage_attrs<8>(std::make_integer_sequence<int, 4>{});
     stage_attrs<kSmallT>(std::make_integer_sequence<int, 4>{});
+    fused_attrs(std::make_integer_sequence<int, 4>{});
     smem_attr(col_kernel<N, C::kCW>, C::kColSmem);
     smem_attr(col_kernel<N, 1>, Cfg<N, 8, 1>::kColSmem);
     smem_attr(row_fwd_kernel<N>, C::kRowSmem);
@@ -798,6 +1151,34 @@ struct Launch {
     if (small_col(nvec)) return col(s, sym, nvec, st);
     launch_pdl(col_solve_kernel<N>, dim3((N / 2) / 8 + 1, nvec), 256, Cfg<N, 8, 1>::kColSmem, st, s, tab, sym,
                twiddle_table(N));
+  }
+  // fused Poisson path: 8-row tiles, P + X only (the x-FFTs run in place)
+  static constexpr size_t kFusSmem = 2 * Cfg<N, 8>::kTileBytes;
+  template <int... S>
+  static void fused_attrs(std::integer_sequence<int, S...>) {
+    (smem_attr(stage_kernel<N, kModeTlm, 8, S, true>, kFusSmem), ...);
+    (smem_attr(stage_kernel<N, kModeAdj, 8, S, true>, kFusSmem), ...);
+  }
+  static void stage_fused(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
+    setup();
+    const dim3 g(N / 8, nvec), b(kThreads);
+    const bool tlm = mode == kModeTlm;
+    if (mode == kModeNl) throw std::invalid_argument("bve_stage: the fused path covers TLM/ADJ");
+    switch (a.stage) {
+      case 0: return launch_pdl(tlm ? stage_kernel<N, kModeTlm, 8, 0, true> : stage_kernel<N, kModeAdj, 8, 0, true>, g, b, kFusSmem, st, a);
+      case 1: return launch_pdl(tlm ? stage_kernel<N, kModeTlm, 8, 1, true> : stage_kernel<N, kModeAdj, 8, 1, true>, g, b, kFusSmem, st, a);
+      case 2: return launch_pdl(tlm ? stage_kernel<N, kModeTlm, 8, 2, true> : stage_kernel<N, kModeAdj, 8, 2, true>, g, b, kFusSmem, st, a);
+      default: return launch_pdl(tlm ? stage_kernel<N, kModeTlm, 8, 3, true> : stage_kernel<N, kModeAdj, 8, 3, true>, g, b, kFusSmem, st, a);
+    }
+  }
+  static void carry(double2* s, const double2* lsum, double2* cc, double2* ce, const double4* tab, const double* sym,
+                    int nvec, cudaStream_t st) {
+    setup();
+    if constexpr (N >= 64) {
+      launch_pdl(carry_kernel<N>, dim3(ceil_div(N / 2, 32) + 1, nvec), 256, 0, st, s, lsum, cc, ce, tab);
+    } else {
+      throw std::invalid_argument("bve_carry: the fused path needs n >= 64");
+    }
   }
   template <int T>
   static void stage_t(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
@@ -853,8 +1234,22 @@ void bve_col(int n, double2* s, const double* sym, int nvec, cudaStream_t st) {
 void bve_col_solve(int n, double2* s, const double4* tab, const double* sym, int nvec, cudaStream_t st) {
   dispatch_n(n, [&](auto c) { Launch<decltype(c)::value>::col_solve(s, tab, sym, nvec, st); });
 }
-void bve_stage(int n, int mode, const StageArgs& a, int nvec, cudaStream_t st) {
-  dispatch_n(n, [&](auto c) { Launch<decltype(c)::value>::stage(mode, a, nvec, st); });
+void bve_stage(int n, int mode, const StageArgs& a, int nvec, cudaStream_t st, bool fused) {
+  if (fused && !bve_fused_ok(n, nvec)) throw std::invalid_argument("bve_stage: block too small for the fused path");
+  dispatch_n(n, [&](auto c) {
+    if (fused) Launch<decltype(c)::value>::stage_fused(mode, a, nvec, st);
+    else Launch<decltype(c)::value>::stage(mode, a, nvec, st);
+  });
+}
+bool bve_fused_ok(int n, int nvec) {
+  if (n < 64 || std::getenv("SDV_NO_FUSE")) return false;
+  bool ok = false;
+  dispatch_n(n, [&](auto c) { ok = !Launch<decltype(c)::value>::small_stage(nvec); });
+  return ok;
+}
+void bve_carry(int n, double2* s, const double2* lsum, double2* car_c, double2* car_e, const double4* tab,
+               const double* sym, int nvec, cudaStream_t st) {
+  dispatch_n(n, [&](auto c) { Launch<decltype(c)::value>::carry(s, lsum, car_c, car_e, tab, sym, nvec, st); });
 }
 void gather_obs(const double* f, long long dim, const long long* idx, int n_obs, const double* w, double* y,
                 long long m, int nvec, cudaStream_t st) {

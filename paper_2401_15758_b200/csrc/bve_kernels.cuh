@@ -9,6 +9,9 @@ enum StageMode { kModeTlm = 0, kModeAdj = 1, kModeNl = 2 };
 enum StageFlags {
   kFlagHasPrev = 1,
   kFlagFinish = 2,
+  // fused Poisson path: s_in already holds final spectra (first TLM stage,
+  // solved by the column pass), no tile-carry correction on load
+  kFlagRawIn = 4,
   // timing experiments only (probe): skip a phase, results are garbage
   kFlagSkipInvFft = 16,
   kFlagSkipStencil = 32,
@@ -38,13 +41,33 @@ struct StageArgs {
   double* store_w = nullptr;
   double* store_p = nullptr;
   const double2* tw = nullptr;
+  // Fused Poisson path (bve_stage(..., fused = true)): s_in/s_out hold the
+  // tile-local recurrence values H of the y-solve (see bve_carry); car_c /
+  // car_e are the tile carries of s_in, lsum receives the tile end values of
+  // s_out; stab = the recurrence table of bve_col_solve. [v][n/8][n/2] double2.
+  const double2* car_c = nullptr;
+  const double2* car_e = nullptr;
+  double2* lsum = nullptr;
+  const double4* stab = nullptr;
   double dt = 0, nu = 0, inv12h2 = 0, invh2 = 0;
 };
 
 void bve_row_fwd(int n, const double* f, double2* s, int nvec, cudaStream_t st);
 void bve_row_inv(int n, const double2* s, double* f, int nvec, cudaStream_t st);
 void bve_col(int n, double2* s, const double* sym, int nvec, cudaStream_t st);
-void bve_stage(int n, int mode, const StageArgs& a, int nvec, cudaStream_t st);
+void bve_stage(int n, int mode, const StageArgs& a, int nvec, cudaStream_t st, bool fused = false);
+// Whether a stage launch over nvec vectors takes the fused Poisson path
+// (8-row tiles; smaller blocks use 2-row tiles and the column pass).
+bool bve_fused_ok(int n, int nvec);
+// Tile carries of the fused Poisson path. The stage kernels leave, per
+// 8-row tile q and x-mode kx >= 1, the zero-carry forward/backward recurrence
+// values H (in s) and the forward end value L_q (in lsum); this pass scans the
+// n/8 tiles of every column (cyclic affine scans) into the carries C_q (from
+// the rows below) and E_q (from the rows above), so that the next stage
+// reconstructs psi_hat = scale (H + alpha_o C_q + rho^(8-o) E_q) on load. The
+// packed kx = 0 column is solved in place by the FFT column path.
+void bve_carry(int n, double2* s, const double2* lsum, double2* car_c, double2* car_e, const double4* tab,
+               const double* sym, int nvec, cudaStream_t st);
 // Poisson column pass by cyclic first-order recurrences (kx >= 1) + the FFT
 // column kernel on the packed kx = 0 column; tab: [n/2] {rho, rho^(n/32),
 // 1/(1-rho^n), h^2 rho/n}; sym: the Poisson spectral symbol (column 0 only).

@@ -195,6 +195,16 @@ Problem::Problem(const ProblemDesc& d, long long n_obs, const long long* idx, co
       tab[4 * kx + 2] = 1.0 / (1.0 - std::pow(rho, n));
       tab[4 * kx + 3] = h * h * rho / n;
     }
+    // entry 0 (kx = 0 is not a recurrence column): the packed column's
+    // constants for the carry pass (col0_warp_solve): x-mode N/2 (d = 6,
+    // rho = 3 - 2 sqrt 2) and the h^2/N scale of the singular x-mode 0
+    {
+      const double rho = 3.0 - 2.0 * std::sqrt(2.0);
+      tab[0] = rho;
+      tab[1] = h * h / n;
+      tab[2] = 1.0 / (1.0 - std::pow(rho, n));
+      tab[3] = h * h * rho / n;
+    }
     solve_tab_.upload(tab.data(), tab.size(), st_);
   }
   SDV_CUDA(cudaStreamSynchronize(st_));
@@ -209,6 +219,25 @@ void Problem::poisson_col(double2* s, int nvec, cudaStream_t st) const {
     bve_col_solve(d_.n, s, reinterpret_cast<const double4*>(solve_tab_.get()), sym_p_.get(), nvec, st);
     count_launch();
   }
+}
+
+bool Problem::fused(int nvec) const { return d_.model == kModelBVE && bve_fused_ok(d_.n, nvec); }
+
+long long fused_stride(int n) { return static_cast<long long>(n / 8) * (n / 2); }
+
+void Problem::poisson_carry(double2* s, long long woff, int nvec, cudaStream_t st) const {
+  const long long fs = fused_stride(d_.n);
+  bve_carry(d_.n, s, lsum_.get() + woff * fs, carc_.get() + woff * fs, care_.get() + woff * fs,
+            reinterpret_cast<const double4*>(solve_tab_.get()), sym_p_.get(), nvec, st);
+  count_launch();
+}
+
+void Problem::set_fused(StageArgs& a, long long woff) const {
+  const long long fs = fused_stride(d_.n);
+  a.car_c = carc_.get() + woff * fs;
+  a.car_e = care_.get() + woff * fs;
+  a.lsum = lsum_.get() + woff * fs;
+  a.stab = reinterpret_cast<const double4*>(solve_tab_.get());
 }
 
 int Problem::group() const {
@@ -232,6 +261,10 @@ void Problem::ensure_work(int nvec) const {
   wx1_.alloc(f);
   ws0_.alloc(static_cast<size_t>(g) * d_.n * (d_.n / 2));
   ws1_.alloc(static_cast<size_t>(g) * d_.n * (d_.n / 2));
+  const size_t fs = static_cast<size_t>(g) * (d_.n / 8) * (d_.n / 2);
+  lsum_.alloc(fs);
+  carc_.alloc(fs);
+  care_.alloc(fs);
   work_nvec_ = g;
 }
 
@@ -456,11 +489,18 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
       bve_row_fwd(n, state + L.v0 * dim_, L.s_cur, L.cnt, L.st);
       count_launch();
     }
+    bool first = true;
     for (int k = k0; k < k1; ++k) {
       for (int s = 0; s < 4; ++s) {
-        // interleave the lanes' launches so their kernels co-reside on SMs
-        for (auto& L : lanes) poisson_col(L.s_cur, L.cnt, L.st);
+        // interleave the lanes' launches so their kernels co-reside on SMs;
+        // fused lanes: the first stage reads column-solved spectra, later
+        // stages the tile-local values + carries
         for (auto& L : lanes) {
+          if (fused(L.cnt) && !first) poisson_carry(L.s_cur, L.woff, L.cnt, L.st);
+          else poisson_col(L.s_cur, L.cnt, L.st);
+        }
+        for (auto& L : lanes) {
+          const bool fz = fused(L.cnt);
           double* dst = state + L.v0 * dim_;
           double* xb[2] = {wx0_.get() + L.woff * dim_, wx1_.get() + L.woff * dim_};
           StageArgs a = bve_args(d_);
@@ -473,10 +513,15 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
           a.acc = wa_.get() + L.woff * dim_;
           a.base_w = tr.w.get() + (static_cast<long long>(k) * 4 + s) * dim_;
           a.base_p = tr.p.get() + (static_cast<long long>(k) * 4 + s) * dim_;
-          bve_stage(n, kModeTlm, a, L.cnt, L.st);
+          if (fz) {
+            set_fused(a, L.woff);
+            if (first) a.flags |= kFlagRawIn;
+          }
+          bve_stage(n, kModeTlm, a, L.cnt, L.st, fz);
           count_launch();
           std::swap(L.s_cur, L.s_nxt);
         }
+        first = false;
       }
       if (y && (k + 1) % d_.spi == 0) {
         const int iv = (k + 1) / d_.spi - 1;
@@ -566,8 +611,12 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
       for (int s = 3; s >= 0; --s) {
         const bool has_prev = !first;
         if (has_prev)
-          for (auto& L : lanes) poisson_col(L.s_cur, L.cnt, L.st);
+          for (auto& L : lanes) {
+            if (fused(L.cnt)) poisson_carry(L.s_cur, L.woff, L.cnt, L.st);
+            else poisson_col(L.s_cur, L.cnt, L.st);
+          }
         for (auto& L : lanes) {
+          const bool fz = fused(L.cnt);
           StageArgs a = bve_args(d_);
           a.stage = s;
           a.flags = has_prev ? kFlagHasPrev : 0;
@@ -579,7 +628,8 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
           a.q_out = (qi ? wx0_.get() : wx1_.get()) + L.woff * dim_;
           a.base_w = tr.w.get() + (static_cast<long long>(k) * 4 + s) * dim_;
           a.base_p = tr.p.get() + (static_cast<long long>(k) * 4 + s) * dim_;
-          bve_stage(n, kModeAdj, a, L.cnt, L.st);
+          if (fz) set_fused(a, L.woff);
+          bve_stage(n, kModeAdj, a, L.cnt, L.st, fz);
           count_launch();
           std::swap(L.s_cur, L.s_nxt);
         }
@@ -588,14 +638,17 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
       }
     }
     for (auto& L : lanes) {
-      poisson_col(L.s_cur, L.cnt, L.st);
+      const bool fz = fused(L.cnt);
+      if (fz) poisson_carry(L.s_cur, L.woff, L.cnt, L.st);
+      else poisson_col(L.s_cur, L.cnt, L.st);
       StageArgs a = bve_args(d_);
       a.flags = kFlagHasPrev | kFlagFinish;
       a.s_in = L.s_cur;
       a.d = state + L.v0 * dim_;
       a.acc = wa_.get() + L.woff * dim_;
       a.q_in = (qi ? wx1_.get() : wx0_.get()) + L.woff * dim_;
-      bve_stage(n, kModeAdj, a, L.cnt, L.st);
+      if (fz) set_fused(a, L.woff);
+      bve_stage(n, kModeAdj, a, L.cnt, L.st, fz);
       count_launch();
     }
     join_lanes(lanes);
@@ -638,10 +691,12 @@ void Problem::probe_stage_kernels(const Trajectory& tr, int s, int stages, float
     double2* s_cur = ws0_.get();
     double2* s_nxt = ws1_.get();
     bve_row_fwd(n, dst, s_cur, s, st_);
+    const bool fz = fused(s);
     for (int q = 0; q < stages; ++q) {
       const int k = (q / 4) % tr.steps, sg = q % 4;
       SDV_CUDA(cudaEventRecord(ev[0], st_));
-      poisson_col(s_cur, s, st_);
+      if (fz && q > 0) poisson_carry(s_cur, 0, s, st_);
+      else poisson_col(s_cur, s, st_);
       SDV_CUDA(cudaEventRecord(ev[1], st_));
       StageArgs a = bve_args(d_);
       a.stage = sg;
@@ -655,7 +710,11 @@ void Problem::probe_stage_kernels(const Trajectory& tr, int s, int stages, float
       a.acc = wa_.get();
       a.base_w = tr.w.get() + (static_cast<long long>(k) * 4 + sg) * dim_;
       a.base_p = tr.p.get() + (static_cast<long long>(k) * 4 + sg) * dim_;
-      bve_stage(n, kModeTlm, a, s, st_);
+      if (fz) {
+        set_fused(a, 0);
+        if (q == 0) a.flags |= kFlagRawIn;
+      }
+      bve_stage(n, kModeTlm, a, s, st_, fz);
       SDV_CUDA(cudaEventRecord(ev[2], st_));
       SDV_CUDA(cudaEventSynchronize(ev[2]));
       float m1 = 0, m2 = 0;

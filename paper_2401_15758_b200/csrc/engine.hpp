@@ -110,6 +110,11 @@ class Problem {
   // Poisson column pass on row spectra (recurrence solver; SDV_COL_FFT=1 selects
   // the y-FFT / multiply / inverse y-FFT kernel instead).
   void poisson_col(double2* s, int nvec, cudaStream_t st) const;
+  // Fused Poisson path (bve_stage fused = true): tile carries of the spectra
+  // in s for the lane's vectors (see bve_carry).
+  void poisson_carry(double2* s, long long woff, int nvec, cudaStream_t st) const;
+  bool fused(int nvec) const;
+  void set_fused(StageArgs& a, long long woff) const;
   // kModelBVE3: model constants, forcing, Poisson and prior DST solvers, and
   // sweep workspace (5 fields per vector)
   Bve3Args b3_;
@@ -125,6 +130,7 @@ class Problem {
   // sweep workspace (grown on demand)
   mutable DevBuf<double> wa_, wx0_, wx1_, wstate_, wy_;
   mutable DevBuf<double2> ws0_, ws1_;
+  mutable DevBuf<double2> lsum_, carc_, care_;  // fused path: [g][n/8][n/2] tile sums / carries
   mutable int work_nvec_ = 0;
   // CUDA graphs of small-block Gram sweeps (PCG / probes replay the same
   // launch sequence on the same buffers every iteration).

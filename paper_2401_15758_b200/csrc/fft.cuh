@@ -20,6 +20,16 @@ namespace sdv {
 
 __host__ __device__ constexpr int ilog2_c(int n) { return n <= 1 ? 0 : 1 + ilog2_c(n >> 1); }
 __host__ __device__ __forceinline__ int fpad(int i) { return i + (i >> 3); }
+// Unpadded in-place layout: XOR-swizzle within aligned groups of 8 elements
+// (16 B each). The stride-8 Stockham stores of 8 consecutive lanes then hit 8
+// distinct 16-byte bank groups, like the padded layout, but a length-N buffer
+// occupies exactly N elements, so a transform can run in place over the rows
+// it reads (no separate scratch buffer).
+__host__ __device__ __forceinline__ int fswz(int i) { return i ^ ((i >> 3) & 7); }
+template <bool SWZ>
+__host__ __device__ __forceinline__ int fidx(int i) {
+  return SWZ ? fswz(i) : fpad(i);
+}
 template <int N>
 struct FftSize {
   static constexpr int kPadded = N + N / 8;  // double2 elements per team buffer
@@ -183,7 +193,9 @@ __host__ __device__ __forceinline__ int fft_out_index(int t, int q, int r) {
 // Threads with active == false only take part in the barriers. The caller
 // must __syncthreads() before reusing buf or reading what store() wrote to
 // shared memory.
-template <int N, bool INV, int PASS = 0, class Load, class Store>
+// SWZ selects the buffer layout: padded (fpad, FftSize<N>::kPadded elements)
+// or swizzled in place (fswz, exactly N elements).
+template <int N, bool INV, int PASS = 0, bool SWZ = false, class Load, class Store>
 __device__ __forceinline__ void fft_team(double2* buf, const double2* __restrict__ tw, int t, bool active, Load& load,
                                          Store& store) {
   using P = FftPass<N, PASS>;
@@ -196,7 +208,7 @@ __device__ __forceinline__ void fft_team(double2* buf, const double2* __restrict
       for (int r = 0; r < R; ++r) {
         const int i = fft_in_index<N, PASS>(t, q, r);
         if constexpr (PASS == 0) v[q * R + r] = load(i);
-        else v[q * R + r] = buf[fpad(i)];
+        else v[q * R + r] = buf[fidx<SWZ>(i)];
       }
     fft_pass_compute<N, PASS, INV>(v, t, tw);
   }
@@ -214,10 +226,10 @@ __device__ __forceinline__ void fft_team(double2* buf, const double2* __restrict
 #pragma unroll
       for (int q = 0; q < G; ++q)
 #pragma unroll
-        for (int r = 0; r < R; ++r) buf[fpad(fft_out_index<N, PASS>(t, q, r))] = v[q * R + r];
+        for (int r = 0; r < R; ++r) buf[fidx<SWZ>(fft_out_index<N, PASS>(t, q, r))] = v[q * R + r];
     }
     __syncthreads();
-    fft_team<N, INV, PASS + 1>(buf, tw, t, active, load, store);
+    fft_team<N, INV, PASS + 1, SWZ>(buf, tw, t, active, load, store);
   }
 }
 
