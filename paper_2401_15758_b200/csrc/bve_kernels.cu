@@ -596,6 +596,19 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
 
   pdl_wait();  // everything below reads what the previous launch wrote
 
+  constexpr int kPairs = R / 2;
+  constexpr bool kTail = FUS && kPairs > C::kTeams;
+  // fused path: inverse x-FFT of row pair pr in place in its P region
+  auto pair_fft = [&](int pr, bool act, auto bar_c) {
+    double* pa = P + (2 * pr) * N;
+    double2* buf = reinterpret_cast<double2*>(pa);
+    auto load = [&](int i) { return buf[i]; };
+    auto store = [&](int i, double2 z) {
+      pa[i] = z.x;
+      pa[i + N] = z.y;
+    };
+    fft_team<N, true, 0, true, decltype(bar_c)::value>(buf, tw, t, act, load, store);
+  };
   if constexpr (FUS) {
     // Phase 0: every global tile read of the launch in flight at once. The
     // stencil input (TLM x_in, ADJ q_in) streams into X by cp.async; the
@@ -647,36 +660,40 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
           for (int o = 0; o < T; ++o) fix(h[1 + o], al[o], pw[T - o], c0, e0);
           fix(h[R - 1], al[0], pw[T], cq, eq);
         }
+        // unpack each row pair (a, b) into the full spectrum of z = a + i b
+        // (pass-0 input of the inverse FFT, natural order, in the pair region)
 #pragma unroll
-        for (int r = 0; r < R; ++r) reinterpret_cast<double2*>(P + r * N)[kx] = h[r];
+        for (int pr = 0; pr < R / 2; ++pr) {
+          double2* z = reinterpret_cast<double2*>(P + (2 * pr) * N);
+          const double2 a = h[2 * pr], b = h[2 * pr + 1];
+          if (kx == 0) {
+            z[0] = make_double2(a.x, b.x);
+            z[N / 2] = make_double2(a.y, b.y);
+          } else {
+            z[kx] = make_double2(a.x - b.y, a.y + b.x);
+            z[N - kx] = make_double2(a.x + b.y, b.x - a.y);
+          }
+        }
       }
     }
     if (xsrc) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
     if (inv) {
       // Phase 1: inverse x-FFT of the R rows, in place (pair region of P).
-      constexpr int kPairs = R / 2;
-#pragma unroll 1
-      for (int b0 = 0; b0 < kPairs; b0 += C::kTeams) {
-        const int pr = b0 + team;
-        const bool act = pr < kPairs;
-        double* pa = P + (2 * pr) * N;
-        double2* buf = reinterpret_cast<double2*>(pa);
-        const double2* ra = buf;
-        const double2* rb = buf + N / 2;
-        auto load = [&](int i) { return unpack_elem<N>(ra, rb, i); };
-        auto store = [&](int i, double2 z) {
-          pa[i] = z.x;
-          pa[i + N] = z.y;
-        };
-        fft_team<N, true, 0, true>(buf, tw, t, act, load, store);
+      // With N = 512 (4 teams) the fifth (halo) pair is a tail round: in the
+      // TLM team 0 runs it under a named barrier while the other warps start
+      // stencil sweep A (which reads X and psi_b, not P); the ADJ runs it here.
+      static_assert(kPairs <= 2 * C::kTeams, "fused path: at most two inverse FFT rounds");
+      pair_fft(team, team < kPairs, std::integral_constant<int, 0>{});
+      __syncthreads();
+      if constexpr (kTail && MODE != kModeTlm) {
+        pair_fft(C::kTeams + team, C::kTeams + team < kPairs, std::integral_constant<int, 0>{});
         __syncthreads();
       }
     }
   }
   // Phase 1: inverse x-FFT of rows y0-1 .. y0+T -> P.
   if (!FUS && has_prev && !(p.flags & kFlagSkipInvFft)) {
-    constexpr int kPairs = R / 2;
 #pragma unroll 1
     for (int b0 = 0; b0 < kPairs; b0 += C::kTeams) {
       const int pr = b0 + team;
@@ -768,6 +785,119 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
   }
   __syncthreads();
 
+  if constexpr (FUS && MODE == kModeTlm) {
+    // Phase 3 (fused TLM): each thread owns two adjacent columns x0, x0+1 of
+    // RPG rows; per window row and field one 16-byte load (x0, x0+1) plus the
+    // two outer neighbours (4 values for 2 points instead of 3 per point).
+    //   A: J(psi_b, X) + nu Lap X (smem X, global psi_b)
+    //   B: + J(P, omega_b), RK4 update (smem P, global omega_b)
+    constexpr int NCP = N / 2, RG = kThreads / NCP, RPG = T / RG;
+    static_assert(RG * NCP == kThreads && RPG * RG == T, "fused TLM stencil mapping");
+    const double js = p.inv12h2, ls = p.invh2, nu = p.nu, dt = p.dt;
+    const int x0 = 2 * (tid % NCP), rg = tid / NCP;
+    const int xm = (x0 - 1) & (N - 1), xq = (x0 + 2) & (N - 1);
+    const int r0 = 1 + rg * RPG;
+    const long long gb0 = static_cast<long long>(y0 + r0 - 1) * N;
+    const long long gbm = static_cast<long long>((y0 + r0 - 2) & (N - 1)) * N;
+    const long long gbp = static_cast<long long>((y0 + r0 - 1 + RPG) & (N - 1)) * N;
+    auto goff = [&](int j) { return j < 0 ? gbm : (j >= RPG ? gbp : gb0 + static_cast<long long>(j) * N); };
+    auto lds = [&](const double* S, int j, double* w) {
+      const double* row = S + (r0 + j) * N;
+      const double2 c = *reinterpret_cast<const double2*>(row + x0);
+      w[0] = row[xm];
+      w[1] = c.x;
+      w[2] = c.y;
+      w[3] = row[xq];
+    };
+    auto ldg = [&](const double* G, int j, double* w) {
+      const double* row = G + goff(j);
+      const double2 c = __ldg(reinterpret_cast<const double2*>(row + x0));
+      w[0] = __ldg(row + xm);
+      w[1] = c.x;
+      w[2] = c.y;
+      w[3] = __ldg(row + xq);
+    };
+    double2 rc[RPG];
+    const long long g0 = off + gb0 + x0;
+    auto sweep = [&](const double* S, const double* G, auto pass_c) {
+      constexpr int pass = decltype(pass_c)::value;
+      double ws[3][4], wg[3][4];  // 3-slot rings (base rows are L1-prefetched)
+      lds(S, -1, ws[0]);
+      lds(S, 0, ws[1]);
+      ldg(G, -1, wg[0]);
+      ldg(G, 0, wg[1]);
+      double2 dn[2] = {}, an[2] = {};
+      auto rkload = [&](int j) {  // RK state of owned row j, one row ahead
+        const long long g = g0 + static_cast<long long>(j) * N;
+        if (stage >= 1 && stage <= 2) dn[j & 1] = *reinterpret_cast<const double2*>(p.d + g);
+        if (stage >= 1) an[j & 1] = *reinterpret_cast<const double2*>(p.acc + g);
+      };
+      if (pass == 1) rkload(0);
+#pragma unroll
+      for (int q = 0; q < RPG; ++q) {
+        const int s0 = q % 3, s1 = (q + 1) % 3, s2 = (q + 2) % 3;
+        lds(S, q + 1, ws[s2]);
+        ldg(G, q + 1, wg[s2]);
+        if (pass == 1 && q + 1 < RPG) rkload(q + 1);
+        double kk[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const double W[3][3] = {{ws[s0][c], ws[s0][c + 1], ws[s0][c + 2]},
+                                  {ws[s1][c], ws[s1][c + 1], ws[s1][c + 2]},
+                                  {ws[s2][c], ws[s2][c + 1], ws[s2][c + 2]}};
+          const double B[3][3] = {{wg[s0][c], wg[s0][c + 1], wg[s0][c + 2]},
+                                  {wg[s1][c], wg[s1][c + 1], wg[s1][c + 2]},
+                                  {wg[s2][c], wg[s2][c + 1], wg[s2][c + 2]}};
+          if (pass == 0) kk[c] = arakawa12(B, W) * js + nu * lap5(W) * ls;
+          else kk[c] = (c ? rc[q].y : rc[q].x) + arakawa12(W, B) * js;
+        }
+        if (pass == 0) {
+          rc[q] = make_double2(kk[0], kk[1]);
+        } else {
+          const long long g = g0 + static_cast<long long>(q) * N;
+          // stage 0: x_in is d itself, already in the X tile
+          const double2 dcur = stage == 0 ? *reinterpret_cast<const double2*>(X + (r0 + q) * N + x0) : dn[q & 1];
+          const double2 acur = an[q & 1];
+          double2 out;
+          if (stage == 0) {
+            *reinterpret_cast<double2*>(p.acc + g) = make_double2(dcur.x + dt / 6.0 * kk[0], dcur.y + dt / 6.0 * kk[1]);
+            out = make_double2(dcur.x + 0.5 * dt * kk[0], dcur.y + 0.5 * dt * kk[1]);
+            *reinterpret_cast<double2*>(p.x_out + g) = out;
+          } else if (stage == 1) {
+            *reinterpret_cast<double2*>(p.acc + g) = make_double2(acur.x + dt / 3.0 * kk[0], acur.y + dt / 3.0 * kk[1]);
+            out = make_double2(dcur.x + 0.5 * dt * kk[0], dcur.y + 0.5 * dt * kk[1]);
+            *reinterpret_cast<double2*>(p.x_out + g) = out;
+          } else if (stage == 2) {
+            *reinterpret_cast<double2*>(p.acc + g) = make_double2(acur.x + dt / 3.0 * kk[0], acur.y + dt / 3.0 * kk[1]);
+            out = make_double2(dcur.x + dt * kk[0], dcur.y + dt * kk[1]);
+            *reinterpret_cast<double2*>(p.x_out + g) = out;
+          } else {
+            out = make_double2(acur.x + dt / 6.0 * kk[0], acur.y + dt / 6.0 * kk[1]);
+            *reinterpret_cast<double2*>(p.d + g) = out;
+          }
+          rc[q] = out;
+        }
+      }
+    };
+    if constexpr (kTail) {
+      if (has_prev && !(p.flags & kFlagSkipInvFft) && team == 0)
+        pair_fft(C::kTeams, true, std::integral_constant<int, 1>{});
+    }
+    if (!(p.flags & kFlagSkipStencil)) {
+      if (pf) prefetch_rows<N, true>(p.base_w, y0 - 1, R, tid, kThreads);
+      sweep(X, p.base_p, std::integral_constant<int, 0>{});
+      if constexpr (kTail) __syncthreads();  // tail pair rows of P complete
+      sweep(P, p.base_w, std::integral_constant<int, 1>{});
+    } else {
+      if constexpr (kTail) __syncthreads();
+#pragma unroll
+      for (int q = 0; q < RPG; ++q) rc[q] = make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < RPG; ++q) *reinterpret_cast<double2*>(P + (r0 + q) * N + x0) = rc[q];
+    __syncthreads();
+  } else {
   // Phase 3: stencils + RK update on owned rows. Each thread walks kCPT
   // columns of kRPG rows with a 3x3 sliding window per field (3 new loads per
   // field per row).
@@ -993,6 +1123,8 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
     for (int q = 0; q < C::kRPG; ++q) P[(r0 + q) * N + xt + cc * C::kNCT] = res[cc][q];
   __syncthreads();
 
+  }
+
   // Phase 4: forward x-FFT of the owned rows -> next row spectra.
   constexpr int kOwnPairs = T / 2;
   if constexpr (FUS) {
@@ -1114,7 +1246,7 @@ struct Launch {
     if (done) return;
     stage_attrs<8>(std::make_integer_sequence<int, 4>{});
     stage_attrs<kSmallT>(std::make_integer_sequence<int, 4>{});
-    fused_attrs(std::make_integer_sequence<int, 4>{});
+    if constexpr (N >= 64) fused_attrs(std::make_integer_sequence<int, 4>{});
     smem_attr(col_kernel<N, C::kCW>, C::kColSmem);
     smem_attr(col_kernel<N, 1>, Cfg<N, 8, 1>::kColSmem);
     smem_attr(row_fwd_kernel<N>, C::kRowSmem);
@@ -1160,6 +1292,13 @@ struct Launch {
     (smem_attr(stage_kernel<N, kModeAdj, 8, S, true>, kFusSmem), ...);
   }
   static void stage_fused(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
+    if constexpr (N < 64) {
+      throw std::invalid_argument("bve_stage: the fused path needs n >= 64");
+    } else {
+      stage_fused_impl(mode, a, nvec, st);
+    }
+  }
+  static void stage_fused_impl(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
     setup();
     const dim3 g(N / 8, nvec), b(kThreads);
     const bool tlm = mode == kModeTlm;

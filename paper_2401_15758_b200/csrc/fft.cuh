@@ -193,9 +193,18 @@ __host__ __device__ __forceinline__ int fft_out_index(int t, int q, int r) {
 // Threads with active == false only take part in the barriers. The caller
 // must __syncthreads() before reusing buf or reading what store() wrote to
 // shared memory.
+// Barrier of fft_team: BAR = 0 synchronises the CTA; BAR > 0 is named
+// barrier BAR over the calling team's N/8 threads only (warp-aligned teams),
+// so one team can run a transform while the rest of the CTA does other work.
+template <int BAR, int COUNT>
+__device__ __forceinline__ void team_sync() {
+  if constexpr (BAR == 0) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(COUNT) : "memory");
+}
+
 // SWZ selects the buffer layout: padded (fpad, FftSize<N>::kPadded elements)
 // or swizzled in place (fswz, exactly N elements).
-template <int N, bool INV, int PASS = 0, bool SWZ = false, class Load, class Store>
+template <int N, bool INV, int PASS = 0, bool SWZ = false, int BAR = 0, class Load, class Store>
 __device__ __forceinline__ void fft_team(double2* buf, const double2* __restrict__ tw, int t, bool active, Load& load,
                                          Store& store) {
   using P = FftPass<N, PASS>;
@@ -213,7 +222,7 @@ __device__ __forceinline__ void fft_team(double2* buf, const double2* __restrict
     fft_pass_compute<N, PASS, INV>(v, t, tw);
   }
   if constexpr (P::LAST) {
-    __syncthreads();  // store() may target buf: all reads of this pass come first
+    team_sync<BAR, N / 8>();  // store() may target buf: all reads of this pass come first
     if (active) {
 #pragma unroll
       for (int q = 0; q < G; ++q)
@@ -221,15 +230,15 @@ __device__ __forceinline__ void fft_team(double2* buf, const double2* __restrict
         for (int r = 0; r < R; ++r) store(fft_out_index<N, PASS>(t, q, r), v[q * R + r]);
     }
   } else {
-    __syncthreads();  // every read of buf in this pass precedes the in-place writes
+    team_sync<BAR, N / 8>();  // every read of buf in this pass precedes the in-place writes
     if (active) {
 #pragma unroll
       for (int q = 0; q < G; ++q)
 #pragma unroll
         for (int r = 0; r < R; ++r) buf[fidx<SWZ>(fft_out_index<N, PASS>(t, q, r))] = v[q * R + r];
     }
-    __syncthreads();
-    fft_team<N, INV, PASS + 1, SWZ>(buf, tw, t, active, load, store);
+    team_sync<BAR, N / 8>();
+    fft_team<N, INV, PASS + 1, SWZ, BAR>(buf, tw, t, active, load, store);
   }
 }
 
