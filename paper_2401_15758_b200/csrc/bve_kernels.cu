@@ -785,8 +785,8 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
   }
   __syncthreads();
 
-  if constexpr (FUS && MODE == kModeTlm) {
-    // Phase 3 (fused TLM): each thread owns two adjacent columns x0, x0+1 of
+  if constexpr (FUS && MODE != kModeNl) {
+    // Phase 3 (fused TLM/ADJ): each thread owns two adjacent columns x0, x0+1 of
     // RPG rows; per window row and field one 16-byte load (x0, x0+1) plus the
     // two outer neighbours (4 values for 2 points instead of 3 per point).
     //   A: J(psi_b, X) + nu Lap X (smem X, global psi_b)
@@ -832,13 +832,13 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
         if (stage >= 1 && stage <= 2) dn[j & 1] = *reinterpret_cast<const double2*>(p.d + g);
         if (stage >= 1) an[j & 1] = *reinterpret_cast<const double2*>(p.acc + g);
       };
-      if (pass == 1) rkload(0);
+      if (MODE == kModeTlm && pass == 1) rkload(0);
 #pragma unroll
       for (int q = 0; q < RPG; ++q) {
         const int s0 = q % 3, s1 = (q + 1) % 3, s2 = (q + 2) % 3;
         lds(S, q + 1, ws[s2]);
         ldg(G, q + 1, wg[s2]);
-        if (pass == 1 && q + 1 < RPG) rkload(q + 1);
+        if (MODE == kModeTlm && pass == 1 && q + 1 < RPG) rkload(q + 1);
         double kk[2];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -848,10 +848,16 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
           const double B[3][3] = {{wg[s0][c], wg[s0][c + 1], wg[s0][c + 2]},
                                   {wg[s1][c], wg[s1][c + 1], wg[s1][c + 2]},
                                   {wg[s2][c], wg[s2][c + 1], wg[s2][c + 2]}};
-          if (pass == 0) kk[c] = arakawa12(B, W) * js + nu * lap5(W) * ls;
+          if (MODE == kModeAdj) kk[c] = pass == 0 ? -arakawa12(B, W) * js + nu * lap5(W) * ls : -arakawa12(W, B) * js;
+          else if (pass == 0) kk[c] = arakawa12(B, W) * js + nu * lap5(W) * ls;
           else kk[c] = (c ? rc[q].y : rc[q].x) + arakawa12(W, B) * js;
         }
-        if (pass == 0) {
+        if (MODE == kModeAdj) {
+          // A: q_out = -J(psi_b, a) + nu Lap a (non-Poisson part of mu);
+          // B: -J(a, omega_b), the next Poisson input
+          if (pass == 0) *reinterpret_cast<double2*>(p.q_out + g0 + static_cast<long long>(q) * N) = make_double2(kk[0], kk[1]);
+          else rc[q] = make_double2(kk[0], kk[1]);
+        } else if (pass == 0) {
           rc[q] = make_double2(kk[0], kk[1]);
         } else {
           const long long g = g0 + static_cast<long long>(q) * N;
@@ -879,17 +885,21 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
         }
       }
     };
-    if constexpr (kTail) {
+    constexpr bool kTlmTail = kTail && MODE == kModeTlm;
+    if constexpr (kTlmTail) {
       if (has_prev && !(p.flags & kFlagSkipInvFft) && team == 0)
         pair_fft(C::kTeams, true, std::integral_constant<int, 1>{});
     }
     if (!(p.flags & kFlagSkipStencil)) {
       if (pf) prefetch_rows<N, true>(p.base_w, y0 - 1, R, tid, kThreads);
       sweep(X, p.base_p, std::integral_constant<int, 0>{});
-      if constexpr (kTail) __syncthreads();  // tail pair rows of P complete
-      sweep(P, p.base_w, std::integral_constant<int, 1>{});
+      if constexpr (kTlmTail) __syncthreads();  // tail pair rows of P complete
+      // ADJ: both sweeps walk X; a barrier keeps the compiler from merging
+      // them into one schedule with both windows live (register spills)
+      if constexpr (MODE == kModeAdj) __syncthreads();
+      sweep(MODE == kModeTlm ? P : X, p.base_w, std::integral_constant<int, 1>{});
     } else {
-      if constexpr (kTail) __syncthreads();
+      if constexpr (kTlmTail) __syncthreads();
 #pragma unroll
       for (int q = 0; q < RPG; ++q) rc[q] = make_double2(0.0, 0.0);
     }
