@@ -607,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
       pa[i] = z.x;
       pa[i + N] = z.y;
     };
-    fft_team<N, true, 0, true, decltype(bar_c)::value>(buf, tw, t, act, load, store);
+    fft_team<N, true, 0, true, decltype(bar_c)::value, true>(buf, tw, t, act, load, store);
   };
   if constexpr (FUS) {
     // Phase 0: every global tile read of the launch in flight at once. The
@@ -1149,7 +1149,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
       double2* buf = reinterpret_cast<double2*>(P + (1 + 2 * pr) * N);
       auto load = [&](int i) { return make_double2(pa[i], pa[i + N]); };
       auto store = [&](int i, double2 z) { buf[fswz(i)] = z; };
-      fft_team<N, false, 0, true>(buf, tw, t, act, load, store);
+      fft_team<N, false, 0, true, 0, true>(buf, tw, t, act, load, store);
       __syncthreads();
     }
     // Tile-local y-recurrences of the next Poisson solve, per x-mode kx

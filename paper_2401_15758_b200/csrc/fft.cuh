@@ -151,7 +151,10 @@ void fft_build_twiddles(int n, Cplx* out, Make make) {
 
 // One Stockham pass for team thread t: 8/R butterflies b = t + (N/8) q.
 // Input index of (q, r): b + r N/R; output index: (b - k) R + k + r NS.
-template <int N, int PASS, bool INV>
+// TWP: radix-8 passes load w^k and w^2k and form w^3k .. w^7k by products
+// (5 complex multiplies instead of 5 more L1 loads; within a few ulp of the
+// exact-rounded table). Used by the L1-bound fused stage kernels.
+template <int N, int PASS, bool INV, bool TWP = false>
 __host__ __device__ __forceinline__ void fft_pass_compute(double2* v, int t, const double2* __restrict__ tw) {
   using P = FftPass<N, PASS>;
   constexpr int R = P::R, G = 8 / R, T = N / 8;
@@ -161,13 +164,31 @@ __host__ __device__ __forceinline__ void fft_pass_compute(double2* v, int t, con
     const int k = b & (P::NS - 1);
     if (P::NS > 1) {
       const double2* twp = tw + P::kTwOff + k;
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
+      if constexpr (R == 8 && TWP) {
 #ifdef __CUDA_ARCH__
-        v[q * R + r] = cmul_tw<INV>(v[q * R + r], __ldg(twp + (r - 1) * P::NS));
+        const double2 w1 = __ldg(twp), w2 = __ldg(twp + P::NS);
 #else
-        v[q * R + r] = cmul_tw<INV>(v[q * R + r], twp[(r - 1) * P::NS]);
+        const double2 w1 = twp[0], w2 = twp[P::NS];
 #endif
+        double2 w[8];
+        w[1] = w1;
+        w[2] = w2;
+        w[3] = cmul_tw<false>(w2, w1);
+        w[4] = cmul_tw<false>(w2, w2);
+        w[5] = cmul_tw<false>(w[4], w1);
+        w[6] = cmul_tw<false>(w[3], w[3]);
+        w[7] = cmul_tw<false>(w[4], w[3]);
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[q * R + r] = cmul_tw<INV>(v[q * R + r], w[r]);
+      } else {
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+#ifdef __CUDA_ARCH__
+          v[q * R + r] = cmul_tw<INV>(v[q * R + r], __ldg(twp + (r - 1) * P::NS));
+#else
+          v[q * R + r] = cmul_tw<INV>(v[q * R + r], twp[(r - 1) * P::NS]);
+#endif
+        }
       }
     }
     dftR<R, INV>(v + q * R);
@@ -204,7 +225,7 @@ __device__ __forceinline__ void team_sync() {
 
 // SWZ selects the buffer layout: padded (fpad, FftSize<N>::kPadded elements)
 // or swizzled in place (fswz, exactly N elements).
-template <int N, bool INV, int PASS = 0, bool SWZ = false, int BAR = 0, class Load, class Store>
+template <int N, bool INV, int PASS = 0, bool SWZ = false, int BAR = 0, bool TWP = false, class Load, class Store>
 __device__ __forceinline__ void fft_team(double2* buf, const double2* __restrict__ tw, int t, bool active, Load& load,
                                          Store& store) {
   using P = FftPass<N, PASS>;
@@ -219,7 +240,7 @@ __device__ __forceinline__ void fft_team(double2* buf, const double2* __restrict
         if constexpr (PASS == 0) v[q * R + r] = load(i);
         else v[q * R + r] = buf[fidx<SWZ>(i)];
       }
-    fft_pass_compute<N, PASS, INV>(v, t, tw);
+    fft_pass_compute<N, PASS, INV, TWP>(v, t, tw);
   }
   if constexpr (P::LAST) {
     team_sync<BAR, N / 8>();  // store() may target buf: all reads of this pass come first
@@ -238,7 +259,7 @@ __device__ __forceinline__ void fft_team(double2* buf, const double2* __restrict
         for (int r = 0; r < R; ++r) buf[fidx<SWZ>(fft_out_index<N, PASS>(t, q, r))] = v[q * R + r];
     }
     team_sync<BAR, N / 8>();
-    fft_team<N, INV, PASS + 1, SWZ, BAR>(buf, tw, t, active, load, store);
+    fft_team<N, INV, PASS + 1, SWZ, BAR, TWP>(buf, tw, t, active, load, store);
   }
 }
 
