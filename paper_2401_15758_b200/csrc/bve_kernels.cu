@@ -23,6 +23,7 @@
 
 #include "bve_kernels.cuh"
 #include "fft.cuh"
+#include "stencil.cuh"
 
 namespace sdv {
 
@@ -83,19 +84,6 @@ __device__ __forceinline__ void pack_pair(const double2* z, double2* __restrict_
   }
 }
 
-// Arakawa Jacobian J(a,b) ~ a_x b_y - a_y b_x from 3x3 neighbourhoods
-// a[dy][dx], b[dy][dx] (dy, dx in {0,1,2} <-> offsets -1, 0, +1); returns 12 h^2 J.
-__device__ __forceinline__ double arakawa12(const double a[3][3], const double b[3][3]) {
-  const double jpp = (a[1][2] - a[1][0]) * (b[2][1] - b[0][1]) - (a[2][1] - a[0][1]) * (b[1][2] - b[1][0]);
-  const double jpx = a[1][2] * (b[2][2] - b[0][2]) - a[1][0] * (b[2][0] - b[0][0]) -
-                     a[2][1] * (b[2][2] - b[2][0]) + a[0][1] * (b[0][2] - b[0][0]);
-  const double jxp = b[2][1] * (a[2][2] - a[2][0]) - b[0][1] * (a[0][2] - a[0][0]) -
-                     b[1][2] * (a[2][2] - a[0][2]) + b[1][0] * (a[2][0] - a[0][0]);
-  return jpp + jpx + jxp;
-}
-__device__ __forceinline__ double lap5(const double o[3][3]) {
-  return o[1][0] + o[1][2] + o[0][1] + o[2][1] - 4.0 * o[1][1];
-}
 // Asynchronous global -> shared 16-byte copy (LDGSTS): every copy of a tile is
 // in flight at once instead of one load-use round trip per element.
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {

@@ -477,6 +477,14 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
     count_launch();
     return;
   }
+  if (bve_cluster_ok(d_.n, nvec)) {
+    const StageArgs b = bve_args(d_);
+    bve_cluster_sweep(d_.n, kModeTlm, state, nvec, tr.w.get(), tr.p.get(), k0, k1, idx_.get(), static_cast<int>(n_obs_),
+                      d_.spi, w, y, m(), reinterpret_cast<const double4*>(solve_tab_.get()), b.dt, b.nu, b.inv12h2,
+                      b.invh2, st_);
+    count_launch();
+    return;
+  }
   ensure_work(nvec);
   const int n = d_.n, g = std::min(nvec, group());
   const long long sdim = static_cast<long long>(n) * (n / 2);
@@ -581,6 +589,14 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
       burgers3_adj(a, state, nvec, st_);
     else
       burgers_adj(a, state, nvec, st_);
+    count_launch();
+    return;
+  }
+  if (bve_cluster_ok(d_.n, nvec)) {
+    const StageArgs b = bve_args(d_);
+    bve_cluster_sweep(d_.n, kModeAdj, state, nvec, tr.w.get(), tr.p.get(), k0, k1, idx_.get(), static_cast<int>(n_obs_),
+                      d_.spi, w, const_cast<double*>(y), m(), reinterpret_cast<const double4*>(solve_tab_.get()), b.dt,
+                      b.nu, b.inv12h2, b.invh2, st_);
     count_launch();
     return;
   }

@@ -154,7 +154,17 @@ void fft_build_twiddles(int n, Cplx* out, Make make) {
 // TWP: radix-8 passes load w^k and w^2k and form w^3k .. w^7k by products
 // (5 complex multiplies instead of 5 more L1 loads; within a few ulp of the
 // exact-rounded table). Used by the L1-bound fused stage kernels.
-template <int N, int PASS, bool INV, bool TWP = false>
+// TSM: the twiddle table is in shared memory (plain loads instead of __ldg).
+template <bool TSM>
+__host__ __device__ __forceinline__ double2 tw_load(const double2* p) {
+#ifdef __CUDA_ARCH__
+  if constexpr (TSM) return *p;
+  else return __ldg(p);
+#else
+  return *p;
+#endif
+}
+template <int N, int PASS, bool INV, bool TWP = false, bool TSM = false>
 __host__ __device__ __forceinline__ void fft_pass_compute(double2* v, int t, const double2* __restrict__ tw) {
   using P = FftPass<N, PASS>;
   constexpr int R = P::R, G = 8 / R, T = N / 8;
@@ -165,11 +175,7 @@ __host__ __device__ __forceinline__ void fft_pass_compute(double2* v, int t, con
     if (P::NS > 1) {
       const double2* twp = tw + P::kTwOff + k;
       if constexpr (R == 8 && TWP) {
-#ifdef __CUDA_ARCH__
-        const double2 w1 = __ldg(twp), w2 = __ldg(twp + P::NS);
-#else
-        const double2 w1 = twp[0], w2 = twp[P::NS];
-#endif
+        const double2 w1 = tw_load<TSM>(twp), w2 = tw_load<TSM>(twp + P::NS);
         double2 w[8];
         w[1] = w1;
         w[2] = w2;
@@ -183,11 +189,7 @@ __host__ __device__ __forceinline__ void fft_pass_compute(double2* v, int t, con
       } else {
 #pragma unroll
         for (int r = 1; r < R; ++r) {
-#ifdef __CUDA_ARCH__
-          v[q * R + r] = cmul_tw<INV>(v[q * R + r], __ldg(twp + (r - 1) * P::NS));
-#else
-          v[q * R + r] = cmul_tw<INV>(v[q * R + r], twp[(r - 1) * P::NS]);
-#endif
+          v[q * R + r] = cmul_tw<INV>(v[q * R + r], tw_load<TSM>(twp + (r - 1) * P::NS));
         }
       }
     }
@@ -225,7 +227,8 @@ __device__ __forceinline__ void team_sync() {
 
 // SWZ selects the buffer layout: padded (fpad, FftSize<N>::kPadded elements)
 // or swizzled in place (fswz, exactly N elements).
-template <int N, bool INV, int PASS = 0, bool SWZ = false, int BAR = 0, bool TWP = false, class Load, class Store>
+template <int N, bool INV, int PASS = 0, bool SWZ = false, int BAR = 0, bool TWP = false, bool TSM = false, class Load,
+          class Store>
 __device__ __forceinline__ void fft_team(double2* buf, const double2* __restrict__ tw, int t, bool active, Load& load,
                                          Store& store) {
   using P = FftPass<N, PASS>;
@@ -240,7 +243,7 @@ __device__ __forceinline__ void fft_team(double2* buf, const double2* __restrict
         if constexpr (PASS == 0) v[q * R + r] = load(i);
         else v[q * R + r] = buf[fidx<SWZ>(i)];
       }
-    fft_pass_compute<N, PASS, INV, TWP>(v, t, tw);
+    fft_pass_compute<N, PASS, INV, TWP, TSM>(v, t, tw);
   }
   if constexpr (P::LAST) {
     team_sync<BAR, N / 8>();  // store() may target buf: all reads of this pass come first
@@ -259,7 +262,7 @@ __device__ __forceinline__ void fft_team(double2* buf, const double2* __restrict
         for (int r = 0; r < R; ++r) buf[fidx<SWZ>(fft_out_index<N, PASS>(t, q, r))] = v[q * R + r];
     }
     team_sync<BAR, N / 8>();
-    fft_team<N, INV, PASS + 1, SWZ, BAR, TWP>(buf, tw, t, active, load, store);
+    fft_team<N, INV, PASS + 1, SWZ, BAR, TWP, TSM>(buf, tw, t, active, load, store);
   }
 }
 

@@ -64,3 +64,30 @@ def test_fused_sub_range_tlm_adj(oracle, sdv):
         for j in (0, 5):
             assert rel(Tg[j], otr.tlm_range(b, e, X[j])) <= 1e-10, (b, e, j)
             assert rel(Ag[j], otr.adj_range(b, e, X[j])) <= 1e-10, (b, e, j)
+
+
+@pytest.mark.parametrize("cfg,steps,spi,s", [(2, 40, -1, 1), (2, 20, 10, 3), (4, 20, 10, 1), (4, 40, -1, 4)])
+def test_cluster_sweeps_match_block_path_and_oracle(oracle, sdv, cfg, steps, spi, s):
+    """Cluster-resident small-block sweeps (bve_cluster.cu, opt-in SDV_CLUSTER)
+    vs the block path and the oracle: misfit apply/adjoint and Gram products."""
+    osc, prob = pair(oracle, cfg, steps, spi)
+    otr = osc.linearize(osc.background)
+    gtr = prob.linearize(osc.background)
+    V = oracle.gaussian_matrix(osc.n, s, 41)
+    W = oracle.gaussian_matrix(osc.m, s, 42)
+    try:
+        os.environ["SDV_CLUSTER"] = "8"
+        HV, Y, Z = gtr.gram(V), gtr.misfit_apply(V), gtr.misfit_adjoint(W)
+        os.environ.pop("SDV_CLUSTER", None)
+        HV0, Y0, Z0 = gtr.gram(V), gtr.misfit_apply(V), gtr.misfit_adjoint(W)
+    finally:
+        os.environ.pop("SDV_CLUSTER", None)
+    for j in range(s):
+        assert rel(HV[j], HV0[j]) <= 1e-12, ("HV vs block path", j)
+        assert rel(Y[j], Y0[j]) <= 1e-12, ("Y vs block path", j)
+        assert rel(Z[j], Z0[j]) <= 1e-12, ("Z vs block path", j)
+        assert abs(Y[j] @ W[j] - V[j] @ Z[j]) <= 1e-10 * np.linalg.norm(V[j]) * np.linalg.norm(W[j])
+    Yo = otr.misfit_apply(V[:1], workers=8)
+    assert rel(Y[0], Yo[0]) <= 1e-10
+    assert rel(HV[0], otr.misfit_adjoint(Yo)[0]) <= 1e-10
+    assert rel(Z[0], otr.misfit_adjoint(W[:1], workers=8)[0]) <= 1e-10
