@@ -347,7 +347,8 @@ def run_ours(args, world, rank, local):
         # the two base stage fields (omega_b, psi_b) once for the group
         alg_bytes = g * 16.0 * ngrid + 2 * 8.0 * ngrid
         dur = ms_stage
-        kname = "bve stage_kernel (fused inverse x-FFT + Arakawa TLM stencil + RK4 update + forward x-FFT)"
+        kname = ("bve stage_kernel, fused Poisson path (y-solved spectra from tile carries, in-place inverse x-FFT, "
+                 "Arakawa TLM stencil + RK4 update, forward x-FFT, tile-local y-recurrences)")
     else:
         g = s
         k = max(1, min(prob.total_steps, probe_stages // 4))
