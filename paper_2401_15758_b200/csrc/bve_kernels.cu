@@ -674,10 +674,8 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
       static_assert(kPairs <= 2 * C::kTeams, "fused path: at most two inverse FFT rounds");
       pair_fft(team, team < kPairs, std::integral_constant<int, 0>{});
       __syncthreads();
-      if constexpr (kTail && MODE != kModeTlm) {
-        pair_fft(C::kTeams + team, C::kTeams + team < kPairs, std::integral_constant<int, 0>{});
-        __syncthreads();
-      }
+      // (ADJ: the tail pair runs under a named barrier at the start of
+      // phase 2, overlapped with the combination of rows 0 .. 2 kTeams - 1)
     }
   }
   // Phase 1: inverse x-FFT of rows y0-1 .. y0+T -> P.
@@ -723,12 +721,11 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
     double2* __restrict__ accp = reinterpret_cast<double2*>(p.acc);
     const bool need_a = finish || stage <= 1 || (stage == 3 && has_prev);
     const bool need_l = !(finish || (stage == 3 && has_prev));
-    constexpr int kRB = R % 5 == 0 ? 5 : (R % 2 == 0 ? 2 : 1);
     const double2 z2 = make_double2(0.0, 0.0);
-#pragma unroll 1
-    for (int x2 = tid; x2 < N / 2; x2 += kThreads) {
-#pragma unroll 1
-      for (int rb = 0; rb < R; rb += kRB) {
+    // one batch of RB rows from rb: all loads first, then the arithmetic
+    auto batch = [&](int x2, int rb, auto rb_c) {
+      constexpr int kRB = decltype(rb_c)::value;
+      {
         double2 qv[kRB], av[kRB], lv[kRB];
         long long go[kRB];
 #pragma unroll
@@ -768,6 +765,26 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
           reinterpret_cast<double2*>(X + r * N)[x2] = a;
         }
       }
+    };
+    constexpr bool kAdjTail = FUS && kTail && MODE == kModeAdj;
+    if constexpr (kAdjTail) {
+      // tail inverse-FFT pair (rows 2 kTeams, 2 kTeams + 1) on team 0 while
+      // the other warps combine the rows of the first round
+      constexpr int kR1 = 2 * C::kTeams;  // rows done by round 1
+      static_assert(kR1 % 4 == 0 && R - kR1 == 2, "ADJ tail layout");
+      const bool inv = has_prev && !(p.flags & kFlagSkipInvFft);
+      if (inv && team == 0) pair_fft(C::kTeams, true, std::integral_constant<int, 1>{});
+      for (int x2 = tid; x2 < N / 2; x2 += kThreads)
+#pragma unroll 1
+        for (int rb = 0; rb < kR1; rb += 4) batch(x2, rb, std::integral_constant<int, 4>{});
+      __syncthreads();  // tail rows of P complete
+      for (int x2 = tid; x2 < N / 2; x2 += kThreads) batch(x2, kR1, std::integral_constant<int, 2>{});
+    } else {
+      constexpr int kRB = R % 5 == 0 ? 5 : (R % 2 == 0 ? 2 : 1);
+#pragma unroll 1
+      for (int x2 = tid; x2 < N / 2; x2 += kThreads)
+#pragma unroll 1
+        for (int rb = 0; rb < R; rb += kRB) batch(x2, rb, std::integral_constant<int, kRB>{});
     }
     if (finish) return;
   }
