@@ -42,7 +42,9 @@ def parse():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--s", type=int, default=0, help="block width (default: the config's sketch size k+p)")
     ap.add_argument("--group", type=int, default=0, help="BVE sweep group size (0 = auto, L2-resident)")
-    ap.add_argument("--sweep", default="", help="extra block widths to report, e.g. 1,8,32")
+    ap.add_argument("--sweep", default="auto",
+                    help="extra block widths to report, e.g. 1,8,32; 'auto' = 1,8,32 for config 3 at N=1 "
+                         "(BASELINE.json configs[3] asks for the s in {1, 8, 32, 110} sweep), 'none' = off")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gn", default="auto",
@@ -375,8 +377,11 @@ def run_ours(args, world, rank, local):
                            "note": "SURVEY.md 8(d) streaming model: HVP/s x B_HVP per GPU"}}
 
     sweep = {}
-    if args.sweep:
-        for sv in [int(x) for x in args.sweep.split(",") if x]:
+    sw = args.sweep
+    if sw == "auto":
+        sw = "1,8,32" if args.config == 3 and world == 1 and not args.window else "none"
+    if sw and sw != "none":
+        for sv in [int(x) for x in sw.split(",") if x]:
             Vs = api.gaussian_matrix(n, sv, rank_seed(rank))
             dVs = api.DeviceBuffer(Vs.nbytes)
             dVs.upload(Vs)
