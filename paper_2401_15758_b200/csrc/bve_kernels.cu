@@ -672,8 +672,10 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
       // TLM team 0 runs it under a named barrier while the other warps start
       // stencil sweep A (which reads X and psi_b, not P); the ADJ runs it here.
       static_assert(kPairs <= 2 * C::kTeams, "fused path: at most two inverse FFT rounds");
-      pair_fft(team, team < kPairs, std::integral_constant<int, 0>{});
-      __syncthreads();
+      pair_fft(team, team < kPairs, std::integral_constant<int, -1>{});
+      // TLM: sweep A reads X and psi_b only; the barrier before sweep B
+      // orders these P rows (and the tail pair's)
+      if (MODE != kModeTlm || !kTail) __syncthreads();
       // (ADJ: the tail pair runs under a named barrier at the start of
       // phase 2, overlapped with the combination of rows 0 .. 2 kTeams - 1)
     }
@@ -798,7 +800,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
     //   B: + J(P, omega_b), RK4 update (smem P, global omega_b)
     constexpr int NCP = N / 2, RG = kThreads / NCP, RPG = T / RG;
     static_assert(RG * NCP == kThreads && RPG * RG == T, "fused TLM stencil mapping");
-    const double js = p.inv12h2, ls = p.invh2, nu = p.nu, dt = p.dt;
+    const double js = p.inv12h2, nls = p.nu * p.invh2, dt = p.dt;
     const int x0 = 2 * (tid % NCP), rg = tid / NCP;
     const int xm = (x0 - 1) & (N - 1), xq = (x0 + 2) & (N - 1);
     const int r0 = 1 + rg * RPG;
@@ -853,8 +855,8 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
           const double B[3][3] = {{wg[s0][c], wg[s0][c + 1], wg[s0][c + 2]},
                                   {wg[s1][c], wg[s1][c + 1], wg[s1][c + 2]},
                                   {wg[s2][c], wg[s2][c + 1], wg[s2][c + 2]}};
-          if (MODE == kModeAdj) kk[c] = pass == 0 ? -arakawa12(B, W) * js + nu * lap5(W) * ls : -arakawa12(W, B) * js;
-          else if (pass == 0) kk[c] = arakawa12(B, W) * js + nu * lap5(W) * ls;
+          if (MODE == kModeAdj) kk[c] = pass == 0 ? fma(-arakawa12(B, W), js, nls * lap5(W)) : -arakawa12(W, B) * js;
+          else if (pass == 0) kk[c] = fma(arakawa12(B, W), js, nls * lap5(W));
           else kk[c] = (c ? rc[q].y : rc[q].x) + arakawa12(W, B) * js;
         }
         if (MODE == kModeAdj) {
@@ -1154,7 +1156,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
       double2* buf = reinterpret_cast<double2*>(P + (1 + 2 * pr) * N);
       auto load = [&](int i) { return make_double2(pa[i], pa[i + N]); };
       auto store = [&](int i, double2 z) { buf[fswz(i)] = z; };
-      fft_team<N, false, 0, true, 0, true>(buf, tw, t, act, load, store);
+      fft_team<N, false, 0, true, -1, true>(buf, tw, t, act, load, store);
       __syncthreads();
     }
     // Tile-local y-recurrences of the next Poisson solve, per x-mode kx

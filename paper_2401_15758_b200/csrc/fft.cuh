@@ -219,10 +219,23 @@ __host__ __device__ __forceinline__ int fft_out_index(int t, int q, int r) {
 // Barrier of fft_team: BAR = 0 synchronises the CTA; BAR > 0 is named
 // barrier BAR over the calling team's N/8 threads only (warp-aligned teams),
 // so one team can run a transform while the rest of the CTA does other work.
+// BAR = -1: every team syncs on its own named barrier 1 + threadIdx.x / COUNT
+// (teams are contiguous thread ranges; sub-warp teams use __syncwarp), so the
+// teams of a CTA run their transforms without waiting for each other.
 template <int BAR, int COUNT>
 __device__ __forceinline__ void team_sync() {
-  if constexpr (BAR == 0) __syncthreads();
-  else asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(COUNT) : "memory");
+  if constexpr (BAR == 0) {
+    __syncthreads();
+  } else if constexpr (BAR < 0) {
+    if constexpr (COUNT < 32) {
+      __syncwarp();
+    } else {
+      const int id = 1 + static_cast<int>(threadIdx.x) / COUNT;
+      asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(COUNT) : "memory");
+    }
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(COUNT) : "memory");
+  }
 }
 
 // SWZ selects the buffer layout: padded (fpad, FftSize<N>::kPadded elements)
