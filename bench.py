@@ -56,15 +56,19 @@ def parse():
     return ap.parse_args()
 
 
-def gn_solve_timing(cfg):
+def gn_solve_timing(cfg, method=None):
     """Wall time of a full gn_solve (device-resident: FWD/evaluate, sketch, PCG,
-    More-Thuente) on BASELINE config `cfg`, with its counters."""
-    from paper_2401_15758_b200 import scenario
+    More-Thuente) on BASELINE config `cfg`, with its counters. `method`
+    overrides the config's sketch (C4 compares Nystrom and SingleView)."""
+    from paper_2401_15758_b200 import api, scenario
 
     sc = scenario.build(cfg)
     sc.problem.synchronize()
+    kw = sc.spec.gn_kwargs()
+    if method is not None:
+        kw["method"] = method
     t0 = time.perf_counter()
-    r = sc.problem.gn_solve(**sc.spec.gn_kwargs())
+    r = sc.problem.gn_solve(**kw)
     dt = time.perf_counter() - t0
     log = r["log"]
     last = log[-1] if len(log) else [0] * 16
@@ -72,9 +76,13 @@ def gn_solve_timing(cfg):
 
     err_a = float(np.linalg.norm(r["analysis"] - sc.truth0) / np.linalg.norm(sc.truth0))
     err_b = float(np.linalg.norm(sc.problem.background - sc.truth0) / np.linalg.norm(sc.truth0))
-    return {"config": sc.spec.name, "seconds": dt, "gn_iterations": int(len(log)), "total_pcg": int(r["summary"][2]),
-            "counters": {"fwd": int(last[11]), "tlm": int(last[12]), "adj": int(last[13]),
-                         "offline_tlm": int(last[14]), "offline_adj": int(last[15])},
+    names = {api.RANDSVD: "randsvd", api.NYSTROM: "nystrom", api.SINGLEVIEW: "singleview"}
+    cnt = {"fwd": int(last[11]), "tlm": int(last[12]), "adj": int(last[13]),
+           "offline_tlm": int(last[14]), "offline_adj": int(last[15])}
+    return {"config": sc.spec.name, "method": names.get(kw["method"], str(kw["method"])), "seconds": dt,
+            "gn_iterations": int(len(log)), "total_pcg": int(r["summary"][2]), "counters": cnt,
+            # model applications including sketch construction (BASELINE configs[4] compares these)
+            "tlm_plus_adj_total": cnt["tlm"] + cnt["adj"] + cnt["offline_tlm"] + cnt["offline_adj"],
             "final_cost": float(r["summary"][0]), "rel_error_analysis": err_a, "rel_error_background": err_b}
 
 
@@ -418,7 +426,12 @@ def run_ours(args, world, rank, local):
             gn = "0,1,2" if world == 1 and not args.window else "none"
         if gn and gn != "none":
             cfgs = [0, 1, 2, 3, 4] if gn == "all" else [int(x) for x in gn.split(",") if x]
-            line["gn_solve"] = [gn_solve_timing(c) for c in cfgs]
+            runs = []
+            for c in cfgs:
+                runs.append(gn_solve_timing(c))
+                if c == 4:  # BASELINE configs[4]: SingleView vs Nystrom on total products
+                    runs.append(gn_solve_timing(4, method=api.SINGLEVIEW))
+            line["gn_solve"] = runs
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
