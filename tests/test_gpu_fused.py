@@ -91,3 +91,28 @@ def test_cluster_sweeps_match_block_path_and_oracle(oracle, sdv, cfg, steps, spi
     assert rel(Y[0], Yo[0]) <= 1e-10
     assert rel(HV[0], otr.misfit_adjoint(Yo)[0]) <= 1e-10
     assert rel(Z[0], otr.misfit_adjoint(W[:1], workers=8)[0]) <= 1e-10
+
+
+@pytest.mark.parametrize("n,s", [(64, 37), (64, 40), (128, 21), (256, 11), (512, 7)])
+def test_fused_vs_column_path_other_grids(sdv, n, s):
+    """Fused path on grids without an oracle case (64^2) and on odd block widths
+    (two unequal sweep lanes): Gram products equal the column-pass path to 1e-12
+    and the misfit pair passes the dot test."""
+    from paper_2401_15758_b200 import api, scenario
+
+    spec = scenario.ConfigSpec(**{**scenario.CONFIGS[2].__dict__, "name": f"bve-{n}", "n": n, "steps": 8, "spi": 4,
+                                  "dt": 0.01 * 128 / n})
+    sc = scenario.build(spec)
+    tr = sc.problem.linearize(sc.problem.background)
+    V = api.gaussian_matrix(sc.problem.n, s, 51)
+    W = api.gaussian_matrix(sc.problem.m, s, 52)
+    try:
+        _no_fuse(False)
+        HV, Y, Z = tr.gram(V), tr.misfit_apply(V), tr.misfit_adjoint(W)
+        _no_fuse(True)
+        HV0 = tr.gram(V)
+    finally:
+        _no_fuse(False)
+    for j in range(s):
+        assert rel(HV[j], HV0[j]) <= 1e-12, j
+        assert abs(Y[j] @ W[j] - V[j] @ Z[j]) <= 1e-10 * np.linalg.norm(V[j]) * np.linalg.norm(W[j])
