@@ -379,7 +379,11 @@ def run_ours(args, world, rank, local):
         if t.get("grid") == spec.n:
             traffic = t["dram_bytes_per_vector"] * g
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": traffic, "kernel": kname, "kernel_ms": dur, "col_kernel_ms": ms_col,
+            "traffic": traffic,
+            # measured DRAM bytes (ncu) over the live launch time: how close the
+            # kernel's actual data movement runs to the HBM peak
+            "traffic_GBs": (traffic / (dur / 1000.0) / 1e9) if traffic else None,
+            "kernel": kname, "kernel_ms": dur, "col_kernel_ms": ms_col,
             "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
             "step_model": {"B_HVP_bytes": b_hvp, "achieved_GBs": step_achieved, "frac": step_achieved / hbm,
                            "note": "SURVEY.md 8(d) streaming model: HVP/s x B_HVP per GPU"}}
