@@ -1391,8 +1391,10 @@ void bve_col_solve(int n, double2* s, const double4* tab, const double* sym, int
   dispatch_n(n, [&](auto c) { Launch<decltype(c)::value>::col_solve(s, tab, sym, nvec, st); });
 }
 void bve_stage(int n, int mode, const StageArgs& a, int nvec, cudaStream_t st, bool fused) {
-  if (fused && !bve_fused_ok(n, nvec)) throw std::invalid_argument("bve_stage: block too small for the fused path");
   dispatch_n(n, [&](auto c) {
+    constexpr int NN = decltype(c)::value;
+    if (fused && (NN < 64 || Launch<NN>::small_stage(nvec)))
+      throw std::invalid_argument("bve_stage: block too small for the fused path");
     if (fused) Launch<decltype(c)::value>::stage_fused(mode, a, nvec, st);
     else Launch<decltype(c)::value>::stage(mode, a, nvec, st);
   });

@@ -504,11 +504,11 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
         // fused lanes: the first stage reads column-solved spectra, later
         // stages the tile-local values + carries
         for (auto& L : lanes) {
-          if (fused(L.cnt) && !first) poisson_carry(L.s_cur, L.woff, L.cnt, L.st);
+          if (L.fz && !first) poisson_carry(L.s_cur, L.woff, L.cnt, L.st);
           else poisson_col(L.s_cur, L.cnt, L.st);
         }
         for (auto& L : lanes) {
-          const bool fz = fused(L.cnt);
+          const bool fz = L.fz;
           double* dst = state + L.v0 * dim_;
           double* xb[2] = {wx0_.get() + L.woff * dim_, wx1_.get() + L.woff * dim_};
           StageArgs a = bve_args(d_);
@@ -551,6 +551,7 @@ std::vector<Problem::Lane> Problem::split_lanes(int v0, int gn) const {
   const bool two = gn >= 2 && !std::getenv("SDV_ONE_LANE");
   if (!two) {
     lanes.push_back(Lane{v0, gn, 0, st_});
+    lanes.back().fz = fused(gn);
     return lanes;
   }
   if (!st2_) SDV_CUDA(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking));
@@ -561,6 +562,7 @@ std::vector<Problem::Lane> Problem::split_lanes(int v0, int gn) const {
   const int a = (gn + 1) / 2;
   lanes.push_back(Lane{v0, a, 0, st_});
   lanes.push_back(Lane{v0 + a, gn - a, a, st2_});
+  for (auto& L : lanes) L.fz = fused(L.cnt);
   return lanes;
 }
 
@@ -628,11 +630,11 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
         const bool has_prev = !first;
         if (has_prev)
           for (auto& L : lanes) {
-            if (fused(L.cnt)) poisson_carry(L.s_cur, L.woff, L.cnt, L.st);
+            if (L.fz) poisson_carry(L.s_cur, L.woff, L.cnt, L.st);
             else poisson_col(L.s_cur, L.cnt, L.st);
           }
         for (auto& L : lanes) {
-          const bool fz = fused(L.cnt);
+          const bool fz = L.fz;
           StageArgs a = bve_args(d_);
           a.stage = s;
           a.flags = has_prev ? kFlagHasPrev : 0;
@@ -654,7 +656,7 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
       }
     }
     for (auto& L : lanes) {
-      const bool fz = fused(L.cnt);
+      const bool fz = L.fz;
       if (fz) poisson_carry(L.s_cur, L.woff, L.cnt, L.st);
       else poisson_col(L.s_cur, L.cnt, L.st);
       StageArgs a = bve_args(d_);

@@ -149,6 +149,7 @@ class Problem {
     cudaStream_t st = nullptr;
     double2* s_cur = nullptr;
     double2* s_nxt = nullptr;
+    bool fz = false;       // fused Poisson path (decided once per sweep)
   };
   std::vector<Lane> split_lanes(int v0, int gn) const;
   void join_lanes(const std::vector<Lane>& lanes) const;
