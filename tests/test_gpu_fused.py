@@ -116,3 +116,19 @@ def test_fused_vs_column_path_other_grids(sdv, n, s):
     for j in range(s):
         assert rel(HV[j], HV0[j]) <= 1e-12, j
         assert abs(Y[j] @ W[j] - V[j] @ Z[j]) <= 1e-10 * np.linalg.norm(V[j]) * np.linalg.norm(W[j])
+
+
+@pytest.mark.parametrize("n,s", [(64, 37), (256, 12), (512, 5)])
+def test_fused_sweeps_bitwise_deterministic(sdv, n, s):
+    """Repeated fused-path Gram sweeps are bitwise identical (no shared-memory
+    races in the in-place FFTs / per-team barriers, deterministic reductions)."""
+    from paper_2401_15758_b200 import api, scenario
+
+    spec = scenario.ConfigSpec(**{**scenario.CONFIGS[2].__dict__, "name": f"bve-{n}", "n": n, "steps": 4, "spi": 2,
+                                  "dt": 0.01 * 128 / n})
+    sc = scenario.build(spec)
+    tr = sc.problem.linearize(sc.problem.background)
+    V = api.gaussian_matrix(sc.problem.n, s, 61)
+    first = tr.gram(V)
+    for _ in range(3):
+        assert np.array_equal(tr.gram(V), first)
