@@ -1181,7 +1181,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
         }
       }
       double2* out = p.s_out + soff + static_cast<long long>(y0) * (N / 2) + kx;
-      if (kx != 0) {
+      if (kx != 0 && !(p.flags & kFlagNoRecur)) {
         const double rho = p.stab[kx].x;
         double2 f = make_double2(0.0, 0.0);
 #pragma unroll
@@ -1307,6 +1307,28 @@ struct Launch {
   static void fused_attrs(std::integer_sequence<int, S...>) {
     (smem_attr(stage_kernel<N, kModeTlm, 8, S, true>, kFusSmem), ...);
     (smem_attr(stage_kernel<N, kModeAdj, 8, S, true>, kFusSmem), ...);
+    if constexpr (kLite) {
+      (smem_attr(stage_kernel<N, kModeTlm, kSmallT, S, true>, kLiteSmem), ...);
+      (smem_attr(stage_kernel<N, kModeAdj, kSmallT, S, true>, kLiteSmem), ...);
+    }
+  }
+  // lite path: the two-column stencil mapping needs N/2 >= 256/T column pairs
+  static constexpr bool kLite = N >= 256;
+  static constexpr size_t kLiteSmem = 2 * Cfg<N, kSmallT>::kTileBytes;
+  static void stage_lite(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
+    if constexpr (kLite) {
+      setup();
+      const dim3 g(N / kSmallT, nvec), b(kThreads);
+      const bool tlm = mode == kModeTlm;
+      switch (a.stage) {
+        case 0: return launch_pdl(tlm ? stage_kernel<N, kModeTlm, kSmallT, 0, true> : stage_kernel<N, kModeAdj, kSmallT, 0, true>, g, b, kLiteSmem, st, a);
+        case 1: return launch_pdl(tlm ? stage_kernel<N, kModeTlm, kSmallT, 1, true> : stage_kernel<N, kModeAdj, kSmallT, 1, true>, g, b, kLiteSmem, st, a);
+        case 2: return launch_pdl(tlm ? stage_kernel<N, kModeTlm, kSmallT, 2, true> : stage_kernel<N, kModeAdj, kSmallT, 2, true>, g, b, kLiteSmem, st, a);
+        default: return launch_pdl(tlm ? stage_kernel<N, kModeTlm, kSmallT, 3, true> : stage_kernel<N, kModeAdj, kSmallT, 3, true>, g, b, kLiteSmem, st, a);
+      }
+    } else {
+      throw std::invalid_argument("bve_stage_lite: needs n >= 256");
+    }
   }
   static void stage_fused(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
     if constexpr (N < 64) {
@@ -1404,6 +1426,17 @@ bool bve_fused_ok(int n, int nvec) {
   bool ok = false;
   dispatch_n(n, [&](auto c) { ok = !Launch<decltype(c)::value>::small_stage(nvec); });
   return ok;
+}
+bool bve_lite_ok(int n, int nvec) {
+  if (n < 256 || nvec < 1 || std::getenv("SDV_NO_LITE")) return false;
+  bool small = false;
+  dispatch_n(n, [&](auto c) { small = Launch<decltype(c)::value>::small_stage(nvec); });
+  return small;
+}
+void bve_stage_lite(int n, int mode, const StageArgs& a, int nvec, cudaStream_t st) {
+  if (!(a.flags & kFlagRawIn) || !(a.flags & kFlagNoRecur))
+    throw std::invalid_argument("bve_stage_lite: needs kFlagRawIn | kFlagNoRecur");
+  dispatch_n(n, [&](auto c) { Launch<decltype(c)::value>::stage_lite(mode, a, nvec, st); });
 }
 void bve_carry(int n, double2* s, const double2* lsum, double2* car_c, double2* car_e, const double4* tab,
                const double* sym, int nvec, cudaStream_t st) {

@@ -12,6 +12,9 @@ enum StageFlags {
   // fused Poisson path: s_in already holds final spectra (first TLM stage,
   // solved by the column pass), no tile-carry correction on load
   kFlagRawIn = 4,
+  // fused kernel used as a plain stage (small blocks): write the packed
+  // spectra of the next Poisson input, no tile-local recurrences
+  kFlagNoRecur = 8,
   // timing experiments only (probe): skip a phase, results are garbage
   kFlagSkipInvFft = 16,
   kFlagSkipStencil = 32,
@@ -59,6 +62,11 @@ void bve_stage(int n, int mode, const StageArgs& a, int nvec, cudaStream_t st, b
 // Whether a stage launch over nvec vectors takes the fused Poisson path
 // (8-row tiles; smaller blocks use 2-row tiles and the column pass).
 bool bve_fused_ok(int n, int nvec);
+// Small blocks on grids >= 256^2: the fused stage kernel with 2-row tiles as a
+// plain stage (in-place x-FFTs, stencil input staged up front), flags must
+// include kFlagRawIn | kFlagNoRecur; the column pass stays.
+bool bve_lite_ok(int n, int nvec);
+void bve_stage_lite(int n, int mode, const StageArgs& a, int nvec, cudaStream_t st);
 // Tile carries of the fused Poisson path. The stage kernels leave, per
 // 8-row tile q and x-mode kx >= 1, the zero-carry forward/backward recurrence
 // values H (in s) and the forward end value L_q (in lsum); this pass scans the

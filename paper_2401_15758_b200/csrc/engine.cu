@@ -525,7 +525,13 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
             set_fused(a, L.woff);
             if (first) a.flags |= kFlagRawIn;
           }
-          bve_stage(n, kModeTlm, a, L.cnt, L.st, fz);
+          if (L.lite) {
+            set_fused(a, L.woff);
+            a.flags |= kFlagRawIn | kFlagNoRecur;
+            bve_stage_lite(n, kModeTlm, a, L.cnt, L.st);
+          } else {
+            bve_stage(n, kModeTlm, a, L.cnt, L.st, fz);
+          }
           count_launch();
           std::swap(L.s_cur, L.s_nxt);
         }
@@ -552,6 +558,7 @@ std::vector<Problem::Lane> Problem::split_lanes(int v0, int gn) const {
   if (!two) {
     lanes.push_back(Lane{v0, gn, 0, st_});
     lanes.back().fz = fused(gn);
+    lanes.back().lite = !lanes.back().fz && d_.model == kModelBVE && bve_lite_ok(d_.n, gn);
     return lanes;
   }
   if (!st2_) SDV_CUDA(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking));
@@ -562,7 +569,10 @@ std::vector<Problem::Lane> Problem::split_lanes(int v0, int gn) const {
   const int a = (gn + 1) / 2;
   lanes.push_back(Lane{v0, a, 0, st_});
   lanes.push_back(Lane{v0 + a, gn - a, a, st2_});
-  for (auto& L : lanes) L.fz = fused(L.cnt);
+  for (auto& L : lanes) {
+    L.fz = fused(L.cnt);
+    L.lite = !L.fz && d_.model == kModelBVE && bve_lite_ok(d_.n, L.cnt);
+  }
   return lanes;
 }
 
@@ -647,7 +657,13 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
           a.base_w = tr.w.get() + (static_cast<long long>(k) * 4 + s) * dim_;
           a.base_p = tr.p.get() + (static_cast<long long>(k) * 4 + s) * dim_;
           if (fz) set_fused(a, L.woff);
-          bve_stage(n, kModeAdj, a, L.cnt, L.st, fz);
+          if (L.lite) {
+            set_fused(a, L.woff);
+            a.flags |= kFlagRawIn | kFlagNoRecur;
+            bve_stage_lite(n, kModeAdj, a, L.cnt, L.st);
+          } else {
+            bve_stage(n, kModeAdj, a, L.cnt, L.st, fz);
+          }
           count_launch();
           std::swap(L.s_cur, L.s_nxt);
         }
@@ -666,7 +682,13 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
       a.acc = wa_.get() + L.woff * dim_;
       a.q_in = (qi ? wx1_.get() : wx0_.get()) + L.woff * dim_;
       if (fz) set_fused(a, L.woff);
-      bve_stage(n, kModeAdj, a, L.cnt, L.st, fz);
+      if (L.lite) {
+        set_fused(a, L.woff);
+        a.flags |= kFlagRawIn | kFlagNoRecur;
+        bve_stage_lite(n, kModeAdj, a, L.cnt, L.st);
+      } else {
+        bve_stage(n, kModeAdj, a, L.cnt, L.st, fz);
+      }
       count_launch();
     }
     join_lanes(lanes);

@@ -150,6 +150,7 @@ class Problem {
     double2* s_cur = nullptr;
     double2* s_nxt = nullptr;
     bool fz = false;       // fused Poisson path (decided once per sweep)
+    bool lite = false;     // small block: fused kernel as a plain stage (column pass kept)
   };
   std::vector<Lane> split_lanes(int v0, int gn) const;
   void join_lanes(const std::vector<Lane>& lanes) const;
