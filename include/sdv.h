@@ -144,6 +144,12 @@ int sdv_thin_qr(sdv_problem* p, int64_t n, int64_t l, const double* y, double* q
 int sdv_sketch(sdv_traj* t, int method, int rank, int rank2, uint64_t seed, double* eig, double* basis,
                int64_t counts[3]);
 
+/* lanczos_sketch(h, rank, start) (proj/src/sketch.cpp:292-389) from a caller
+ * vector start (host, n; nonzero), as first_iterate_study calls it with the
+ * GN right-hand side (proj/src/harness.cpp:590-592). Same outputs as
+ * sdv_sketch. */
+int sdv_lanczos_sketch(sdv_traj* t, int rank, const double* start, double* eig, double* basis, int64_t counts[3]);
+
 /* adaptive_randsvd / adaptive_nystrom / adaptive_singleview
  * (proj/src/sketch.cpp:402-564): start at rank, grow by growth while the
  * cond_estimate probe kappa_sk > eps_sketch, capped at max_rank (rank2: the

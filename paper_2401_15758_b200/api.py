@@ -250,6 +250,16 @@ class Trajectory:
         k = int(counts[2])
         return eig[:k], (basis[:k] if basis is not None else None), counts
 
+    def lanczos(self, rank, start):
+        """lanczos_sketch(h, rank, start) (proj/src/sketch.cpp:292-389) from a given start vector."""
+        eig = np.empty(rank)
+        basis = np.empty((rank, self.problem.n))
+        counts = np.zeros(3, np.int64)
+        check(lib().sdv_lanczos_sketch(self._h, rank, _p(_f64(start)), _p(eig), _p(basis),
+                                       counts.ctypes.data_as(I64)))
+        k = int(counts[2])
+        return eig[:k], basis[:k], counts
+
     def sketch_adaptive(self, method, rank, growth, max_rank, seed, rank2=-1, eps_sketch=1.5):
         """adaptive_{randsvd,nystrom,singleview} (proj/src/sketch.cpp:402-564).
 

@@ -312,6 +312,27 @@ int sdv_sketch(sdv_traj* t, int method, int rank, int rank2, uint64_t seed, doub
   });
 }
 
+int sdv_lanczos_sketch(sdv_traj* t, int rank, const double* start, double* eig, double* basis, int64_t counts[3]) {
+  return guard([&] {
+    need(t, "trajectory");
+    need(start, "start");
+    need(eig, "eig");
+    auto& q = *t->owner->p;
+    sdv::MisfitOp op(q, *t->t);
+    sdv::DevBuf<double> st;
+    st.upload(start, static_cast<size_t>(q.dim()), q.stream());
+    sdv::SketchResult r = sdv::lanczos_sketch(op, rank, st.get());
+    std::memcpy(eig, r.evd.eig.data(), sizeof(double) * r.evd.l);
+    if (basis) r.evd.basis.download(basis, static_cast<size_t>(q.dim()) * r.evd.l, q.stream());
+    SDV_CUDA(cudaStreamSynchronize(q.stream()));
+    if (counts) {
+      counts[0] = r.tlm;
+      counts[1] = r.adj;
+      counts[2] = r.final_rank;
+    }
+  });
+}
+
 int sdv_sketch_adaptive(sdv_traj* t, int method, int rank, int growth, int max_rank, int rank2, double eps_sketch,
                         uint64_t seed, double* eig, double* basis, int64_t counts[5], double* kappa, int max_kappa) {
   return guard([&] {
