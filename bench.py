@@ -94,6 +94,15 @@ def dist_env():
     return world, rank, local
 
 
+def local_device(local):
+    """GPU of a local rank: one per rank; with fewer visible GPUs than ranks
+    (a functional run on a 1-GPU box) ranks share them round-robin."""
+    import torch
+
+    n = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    return local % n if n > 0 else local
+
+
 def dist_init(world, backend=None):
     if world <= 1:
         return None
@@ -101,9 +110,12 @@ def dist_init(world, backend=None):
     import torch.distributed as dist
 
     if backend is None:
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
-    if backend == "nccl":
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        # NCCL needs one GPU per rank; with fewer GPUs than ranks (functional
+        # runs) the barrier and the max-over-ranks timing go through gloo
+        ngpu = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        backend = "nccl" if ngpu >= world else "gloo"
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local_device(int(os.environ.get("LOCAL_RANK", "0"))))
     dist.init_process_group(backend=backend)
     return dist
 
@@ -275,10 +287,22 @@ def run_reference(args, world, rank):
 
 
 def config_block(spec, s, group):
+    # bytes one block sweep streams: the stored base trajectory (BVE: omega and
+    # psi per RK4 stage; Burgers: the stage inputs) + the block's RK workspace
+    from paper_2401_15758_b200 import api
+
+    bve = spec.model == api.MODEL_BVE
+    field = 8.0 * spec.dim
+    base = (2 if bve else 1) * 4 * spec.steps * field
+    work = s * (6 if bve else 2) * field
+    l2 = 126e6
+    note = (f"inputs larger than L2: {base / 1e9:.3g} GB base trajectory + {work / 1e9:.3g} GB block workspace "
+            f"streamed per sweep (L2 126 MB)" if base + work > l2 else
+            f"on-chip problem: {(base + work) / 1e6:.3g} MB per sweep fits the 126 MB L2")
     return {"workload": f"{spec.name}: block of s={s} GN Hessian products (TLM+ADJ), BASELINE.json configs",
             "model": spec.name, "grid": spec.n, "rk4_steps": spec.steps, "block_s": s,
             "global_batch": s, "seq_len": spec.steps, "parallelism": "sketch-column sharding (weak)",
-            "sweep_group": group, "l2": "inputs larger than L2 (base trajectory >= 0.8 GB streamed per sweep)"}
+            "sweep_group": group, "l2": note}
 
 
 # ------------------------------------------------------------------ ours ----
@@ -289,7 +313,7 @@ def run_ours(args, world, rank, local):
     from paper_2401_15758_b200 import api, scenario
 
     dist = dist_init(world)
-    sdv.init(local)
+    sdv.init(local_device(local))
     spec = scenario.CONFIGS[args.config]
     if args.window:
         spec = scenario.with_window(spec, steps=args.window, spi=max(1, args.window // 2))
