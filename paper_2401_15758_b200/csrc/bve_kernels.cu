@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
       prefetch_rows<N, true>(p.base_p, y0 - 1, R, tid, kThreads);
       if (!FUS) prefetch_rows<N, false>(p.x_in + off, y0 - 1, R, tid, kThreads);
       if (stage >= 1 && stage <= 2) prefetch_rows<N, false>(p.d + off, y0, T, tid, kThreads);
-      if (stage >= 1) prefetch_rows<N, false>(p.acc + off, y0, T, tid, kThreads);
+      if (stage >= (FUS ? 2 : 1)) prefetch_rows<N, false>(p.acc + off, y0, T, tid, kThreads);
     } else if (MODE == kModeAdj && !finish) {
       prefetch_rows<N, true>(p.base_p, y0 - 1, R, tid, kThreads);
       if (has_prev && !FUS) prefetch_rows<N, false>(p.q_in + off, y0 - 1, R, tid, kThreads);
@@ -837,7 +837,8 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
       auto rkload = [&](int j) {  // RK state of owned row j, one row ahead
         const long long g = g0 + static_cast<long long>(j) * N;
         if (stage >= 1 && stage <= 2) dn[j & 1] = *reinterpret_cast<const double2*>(p.d + g);
-        if (stage >= 1) an[j & 1] = *reinterpret_cast<const double2*>(p.acc + g);
+        // (fused TLM: stage 1 rebuilds the accumulator from d and its input)
+        if (stage >= 2) an[j & 1] = *reinterpret_cast<const double2*>(p.acc + g);
       };
       if (MODE == kModeTlm && pass == 1) rkload(0);
 #pragma unroll
@@ -873,11 +874,14 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
           const double2 acur = an[q & 1];
           double2 out;
           if (stage == 0) {
-            *reinterpret_cast<double2*>(p.acc + g) = make_double2(dcur.x + dt / 6.0 * kk[0], dcur.y + dt / 6.0 * kk[1]);
+            // no accumulator write: with x1 = d + dt/2 k1 (this stage's
+            // output), d + dt/6 k1 = (2 d + x1) / 3, rebuilt in stage 1
             out = make_double2(dcur.x + 0.5 * dt * kk[0], dcur.y + 0.5 * dt * kk[1]);
             *reinterpret_cast<double2*>(p.x_out + g) = out;
           } else if (stage == 1) {
-            *reinterpret_cast<double2*>(p.acc + g) = make_double2(acur.x + dt / 3.0 * kk[0], acur.y + dt / 3.0 * kk[1]);
+            const double2 x1 = *reinterpret_cast<const double2*>(X + (r0 + q) * N + x0);  // this stage's input
+            const double2 a1 = make_double2((2.0 * dcur.x + x1.x) / 3.0, (2.0 * dcur.y + x1.y) / 3.0);
+            *reinterpret_cast<double2*>(p.acc + g) = make_double2(a1.x + dt / 3.0 * kk[0], a1.y + dt / 3.0 * kk[1]);
             out = make_double2(dcur.x + 0.5 * dt * kk[0], dcur.y + 0.5 * dt * kk[1]);
             *reinterpret_cast<double2*>(p.x_out + g) = out;
           } else if (stage == 2) {
