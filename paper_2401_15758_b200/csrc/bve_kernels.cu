@@ -736,7 +736,10 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
           go[u] = (off + static_cast<long long>((y0 - 1 + r) & (N - 1)) * N) / 2 + x2;
           if (FUS) qv[u] = has_prev ? reinterpret_cast<const double2*>(X + r * N)[x2] : z2;  // staged
           else qv[u] = has_prev ? qin[go[u]] : z2;
-          av[u] = need_a ? accp[go[u]] : z2;
+          // the accumulator enters a (halo rows) only at stage 3; stages 1, 0
+          // and the finish update it on the owned rows alone
+          const bool own_r = r >= 1 && r <= T;
+          av[u] = (need_a && (stage == 3 || own_r)) ? accp[go[u]] : z2;
           lv[u] = need_l ? lamp[go[u]] : z2;
         }
 #pragma unroll
