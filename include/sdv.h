@@ -84,6 +84,13 @@ const char* sdv_version(void);
 int sdv_device_init(int device);
 /* Number of kernels this library has launched so far (process-wide). */
 unsigned long long sdv_launch_count(void);
+/* Per-variant launch counters of the sweep kernels (process-wide, atomic):
+ * out[i] for i < min(n, count), returns count; sdv_path_name(i) names
+ * variant i ("bve_stage_fused", "bve_carry", "bve_stage_lite", ...). A CUDA
+ * graph replay is counted once, when it is captured. Lets callers and tests
+ * assert which kernel path a call took. */
+int sdv_path_counts(uint64_t* out, int n);
+const char* sdv_path_name(int i);
 
 /* AssimilationProblem (proj/include/sketchdav/fourdvar.hpp:25-40) + validate
  * (proj/src/fourdvar.cpp:25-58). obs_values/obs_variances: n_obs x n_t

@@ -3,6 +3,11 @@
 // /root/reference/proj/src/linalg.cpp without Eigen.
 #include "oracle.hpp"
 
+#include <condition_variable>
+#include <cstdlib>
+#include <mutex>
+#include <thread>
+
 #include <algorithm>
 #include <limits>
 #include <numeric>
@@ -483,17 +488,103 @@ void fft_inplace(std::vector<cplx>& xv, bool inverse) {
 }
 
 void fft2_inplace(std::vector<cplx>& x, int nx, int ny, bool inverse) {
-  std::vector<cplx> row(static_cast<size_t>(nx)), col(static_cast<size_t>(ny));
-  for (int j = 0; j < ny; ++j) {
-    std::copy(x.begin() + static_cast<size_t>(j) * nx, x.begin() + static_cast<size_t>(j + 1) * nx, row.begin());
-    fft_inplace(row, inverse);
-    std::copy(row.begin(), row.end(), x.begin() + static_cast<size_t>(j) * nx);
+  par_for(ny, [&](int64_t j0, int64_t j1) {
+    std::vector<cplx> row(static_cast<size_t>(nx));
+    for (int64_t j = j0; j < j1; ++j) {
+      std::copy(x.begin() + static_cast<size_t>(j) * nx, x.begin() + static_cast<size_t>(j + 1) * nx, row.begin());
+      fft_inplace(row, inverse);
+      std::copy(row.begin(), row.end(), x.begin() + static_cast<size_t>(j) * nx);
+    }
+  });
+  par_for(nx, [&](int64_t i0, int64_t i1) {
+    std::vector<cplx> col(static_cast<size_t>(ny));
+    for (int64_t i = i0; i < i1; ++i) {
+      for (int j = 0; j < ny; ++j) col[j] = x[i + static_cast<size_t>(nx) * j];
+      fft_inplace(col, inverse);
+      for (int j = 0; j < ny; ++j) x[i + static_cast<size_t>(nx) * j] = col[j];
+    }
+  });
+}
+
+// ------------------------------------------------------------ par_for pool --
+namespace {
+thread_local bool t_no_par = false;
+struct Pool {
+  // Workers spin briefly on the generation counter before sleeping, so a
+  // parallel region costs ~1 us to dispatch (the oracle issues thousands).
+  int nt = 1;
+  std::vector<std::thread> th;
+  std::mutex busy;  // one parallel region at a time
+  std::mutex mu;
+  std::condition_variable cv;
+  std::atomic<uint64_t> gen{0};
+  std::atomic<int> pending{0};
+  std::atomic<bool> stop{false};
+  int64_t n = 0;
+  const std::function<void(int64_t, int64_t)>* f = nullptr;
+  Pool() {
+    if (const char* e = std::getenv("ORACLE_THREADS")) nt = std::max(1, std::atoi(e));
+    for (int t = 1; t < nt; ++t) th.emplace_back([this, t] { worker(t); });
   }
-  for (int i = 0; i < nx; ++i) {
-    for (int j = 0; j < ny; ++j) col[j] = x[i + static_cast<size_t>(nx) * j];
-    fft_inplace(col, inverse);
-    for (int j = 0; j < ny; ++j) x[i + static_cast<size_t>(nx) * j] = col[j];
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> l(mu);
+      stop = true;
+      gen.fetch_add(1);
+    }
+    cv.notify_all();
+    for (auto& x : th) x.join();
   }
+  void chunk(int t) {
+    const int64_t b = n * t / nt, e = n * (t + 1) / nt;
+    if (b < e) (*f)(b, e);
+  }
+  void worker(int t) {
+    t_no_par = true;
+    uint64_t seen = 0;
+    for (;;) {
+      int spins = 0;
+      while (gen.load(std::memory_order_acquire) == seen && ++spins < 20000) {
+      }
+      if (gen.load(std::memory_order_acquire) == seen) {
+        std::unique_lock<std::mutex> l(mu);
+        cv.wait(l, [&] { return gen.load() != seen; });
+      }
+      seen = gen.load(std::memory_order_acquire);
+      if (stop) return;
+      chunk(t);
+      pending.fetch_sub(1, std::memory_order_acq_rel);
+    }
+  }
+  void run(int64_t nn, const std::function<void(int64_t, int64_t)>& ff) {
+    n = nn;
+    f = &ff;
+    pending.store(nt - 1, std::memory_order_relaxed);
+    {
+      std::lock_guard<std::mutex> l(mu);
+      gen.fetch_add(1, std::memory_order_release);
+    }
+    cv.notify_all();
+    chunk(0);
+    while (pending.load(std::memory_order_acquire) != 0) {
+    }
+  }
+};
+Pool& pool() {
+  static Pool p;
+  return p;
+}
+}  // namespace
+
+void set_no_par(bool v) { t_no_par = v; }
+
+void par_for(int64_t n, const std::function<void(int64_t, int64_t)>& f) {
+  if (n <= 0) return;
+  if (t_no_par || n < 2) return f(0, n);
+  Pool& p = pool();
+  if (p.nt <= 1 || !p.busy.try_lock()) return f(0, n);
+  std::lock_guard<std::mutex> l(p.busy, std::adopt_lock);
+  p.run(n, f);
 }
 
 // ---------------------------------------------------- maps, Woodbury, PCG ---

@@ -204,7 +204,8 @@ Vec PeriodicBVE::arakawa(const Vec& a, const Vec& b) const {
   Vec o(static_cast<size_t>(n) * n);
   auto A = [&](int i, int j) { return a[wrap(i, n) + static_cast<size_t>(n) * wrap(j, n)]; };
   auto B = [&](int i, int j) { return b[wrap(i, n) + static_cast<size_t>(n) * wrap(j, n)]; };
-  for (int j = 0; j < n; ++j)
+  par_for(n, [&](int64_t j0, int64_t j1) {
+  for (int j = static_cast<int>(j0); j < j1; ++j)
     for (int i = 0; i < n; ++i) {
       const double jpp = (A(i + 1, j) - A(i - 1, j)) * (B(i, j + 1) - B(i, j - 1)) -
                          (A(i, j + 1) - A(i, j - 1)) * (B(i + 1, j) - B(i - 1, j));
@@ -218,6 +219,7 @@ Vec PeriodicBVE::arakawa(const Vec& a, const Vec& b) const {
                          B(i - 1, j) * (A(i - 1, j + 1) - A(i - 1, j - 1));
       o[i + static_cast<size_t>(n) * j] = (jpp + jpx + jxp) * s;
     }
+  });
   return o;
 }
 
@@ -225,13 +227,15 @@ Vec PeriodicBVE::laplacian(const Vec& f) const {
   const int n = n_;
   const double h = 2.0 * M_PI / n, c = 1.0 / (h * h);
   Vec o(static_cast<size_t>(n) * n);
-  for (int j = 0; j < n; ++j)
+  par_for(n, [&](int64_t j0, int64_t j1) {
+  for (int j = static_cast<int>(j0); j < j1; ++j)
     for (int i = 0; i < n; ++i) {
       const size_t id = i + static_cast<size_t>(n) * j;
       o[id] = (f[wrap(i + 1, n) + static_cast<size_t>(n) * j] + f[wrap(i - 1, n) + static_cast<size_t>(n) * j] +
                f[i + static_cast<size_t>(n) * wrap(j + 1, n)] + f[i + static_cast<size_t>(n) * wrap(j - 1, n)] -
                4.0 * f[id]) * c;
     }
+  });
   return o;
 }
 

@@ -83,6 +83,15 @@ void sym_eig(const Mat& a, Vec& evals, Mat& evecs);
 // Lower-triangular solve L X = B.
 Mat lower_solve(const Mat& l, const Mat& b);
 
+// ---- intra-operator threading (speed only; results are bitwise identical) --
+// par_for(n, f) calls f(b, e) on a static partition of [0, n) over
+// ORACLE_THREADS threads (default 1 = serial). Every output element is computed
+// by exactly the same arithmetic whichever thread owns it, and reductions stay
+// serial, so threading never changes a bit. Serial inside apply_columns
+// workers (no nested oversubscription) and when the pool is busy.
+void par_for(int64_t n, const std::function<void(int64_t, int64_t)>& f);
+void set_no_par(bool v);  // this thread: run par_for serially
+
 // ---- FFT (radix-2, power-of-two lengths) -----------------------------------
 void fft_inplace(std::vector<cplx>& x, bool inverse);  // unnormalised
 void fft2_inplace(std::vector<cplx>& x, int nx, int ny, bool inverse);

@@ -61,6 +61,8 @@ def lib():
         "sdv_version": (C.c_char_p, []),
         "sdv_device_init": (C.c_int, [C.c_int]),
         "sdv_launch_count": (C.c_ulonglong, []),
+        "sdv_path_counts": (C.c_int, [C.POINTER(C.c_uint64), C.c_int]),
+        "sdv_path_name": (C.c_char_p, [C.c_int]),
         "sdv_problem_create": (C.c_int, [C.POINTER(ProblemDesc), C.c_int64, I64, D, D, D, C.POINTER(vp)]),
         "sdv_problem_destroy": (None, [vp]),
         "sdv_problem_dims": (C.c_int, [vp, I64]),

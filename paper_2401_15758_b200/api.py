@@ -41,6 +41,22 @@ def launch_count():
     return int(lib().sdv_launch_count())
 
 
+def path_counts():
+    """Launch counts per sweep-kernel variant ({"bve_stage_fused": k, ...}),
+    process-wide: which kernel path the calls so far took (sdv_path_counts)."""
+    L = lib()
+    n = L.sdv_path_counts(None, 0)
+    buf = (C.c_uint64 * n)()
+    L.sdv_path_counts(buf, n)
+    return {L.sdv_path_name(i).decode(): int(buf[i]) for i in range(n)}
+
+
+def path_delta(before):
+    """Per-variant launches since a path_counts() snapshot."""
+    now = path_counts()
+    return {k: now[k] - before.get(k, 0) for k in now}
+
+
 def mix_seed(seed, stream):
     return int(lib().sdv_mix_seed(seed, stream))
 
@@ -86,6 +102,7 @@ class Problem:
         self.background = bg.copy()
         self.obs_indices = idx.copy()
         self.obs_values = vals.reshape(self.n_t, self.n_obs).copy()
+        self.obs_variances = var.reshape(self.n_t, self.n_obs).copy()
 
     @property
     def handle(self):

@@ -246,12 +246,12 @@ template <int N>
 void spectral1d_launch(const double* in, double* out, const double* sym, int nvec, cudaStream_t st) {
   constexpr int kTeam = FftSize<N>::kTeam;
   const size_t smem = sizeof(double2) * FftSize<N>::kPadded;
-  static bool init = false;
-  if (!init) {
+  static const bool init = [&] {  // thread-safe one-time attribute (magic static)
     SDV_CUDA(cudaFuncSetAttribute(spectral1d_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
-    init = true;
-  }
+    return true;
+  }();
+  (void)init;
   spectral1d_kernel<N><<<nvec, kTeam, smem, st>>>(in, out, sym, twiddle_table(N));
   SDV_LAUNCH_CHECK();
 }

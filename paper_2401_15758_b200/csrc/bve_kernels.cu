@@ -23,6 +23,7 @@
 
 #include "bve_kernels.cuh"
 #include "fft.cuh"
+#include "linalg_kernels.cuh"
 #include "stencil.cuh"
 
 namespace sdv {
@@ -1266,8 +1267,13 @@ struct Launch {
     SDV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
   }
   static void setup() {
-    static bool done = false;
-    if (done) return;
+    static const bool once = [] {  // thread-safe one-time kernel attributes (magic static)
+      setup_once();
+      return true;
+    }();
+    (void)once;
+  }
+  static void setup_once() {
     stage_attrs<8>(std::make_integer_sequence<int, 4>{});
     stage_attrs<kSmallT>(std::make_integer_sequence<int, 4>{});
     if constexpr (N >= 64) fused_attrs(std::make_integer_sequence<int, 4>{});
@@ -1275,7 +1281,6 @@ struct Launch {
     smem_attr(col_kernel<N, 1>, Cfg<N, 8, 1>::kColSmem);
     smem_attr(row_fwd_kernel<N>, C::kRowSmem);
     smem_attr(row_inv_kernel<N>, C::kRowSmem);
-    done = true;
   }
   static void row_fwd(const double* f, double2* s, int nvec, cudaStream_t st) {
     setup();
@@ -1289,6 +1294,7 @@ struct Launch {
   }
   static void col(double2* s, const double* sym, int nvec, cudaStream_t st) {
     setup();
+    count_path(kPathBveColFft);
     if (small_col(nvec)) {
       launch_pdl(col_kernel<N, 1>, dim3(N / 2, nvec), C::kTeam, Cfg<N, 8, 1>::kColSmem, st, s, sym,
                  twiddle_table(N));
@@ -1305,6 +1311,7 @@ struct Launch {
     // CTAs per vector would leave most SMs idle; the 1-column FFT kernel has
     // N/2 CTAs per vector.
     if (small_col(nvec)) return col(s, sym, nvec, st);
+    count_path(kPathBveColSolve);
     launch_pdl(col_solve_kernel<N>, dim3((N / 2) / 8 + 1, nvec), 256, Cfg<N, 8, 1>::kColSmem, st, s, tab, sym,
                twiddle_table(N));
   }
@@ -1325,6 +1332,7 @@ struct Launch {
   static void stage_lite(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
     if constexpr (kLite) {
       setup();
+      count_path(kPathBveStageLite);
       const dim3 g(N / kSmallT, nvec), b(kThreads);
       const bool tlm = mode == kModeTlm;
       switch (a.stage) {
@@ -1346,6 +1354,7 @@ struct Launch {
   }
   static void stage_fused_impl(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
     setup();
+    count_path(kPathBveStageFused);
     const dim3 g(N / 8, nvec), b(kThreads);
     const bool tlm = mode == kModeTlm;
     if (mode == kModeNl) throw std::invalid_argument("bve_stage: the fused path covers TLM/ADJ");
@@ -1360,6 +1369,7 @@ struct Launch {
                     int nvec, cudaStream_t st) {
     setup();
     if constexpr (N >= 64) {
+      count_path(kPathBveCarry);
       launch_pdl(carry_kernel<N>, dim3(ceil_div(N / 2, 32) + 1, nvec), 256, 0, st, s, lsum, cc, ce, tab);
     } else {
       throw std::invalid_argument("bve_carry: the fused path needs n >= 64");
@@ -1389,6 +1399,7 @@ struct Launch {
   }
   static void stage(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
     setup();
+    count_path(kPathBveStagePlain);
     if (small_stage(nvec)) stage_t<kSmallT>(mode, a, nvec, st);
     else stage_t<8>(mode, a, nvec, st);
   }

@@ -81,15 +81,6 @@ void bve_carry(int n, double2* s, const double2* lsum, double2* car_c, double2* 
 // 1/(1-rho^n), h^2 rho/n}; sym: the Poisson spectral symbol (column 0 only).
 void bve_col_solve(int n, double2* s, const double4* tab, const double* sym, int nvec, cudaStream_t st);
 
-// Cluster-resident sweeps for small blocks (bve_cluster.cu): one thread-block
-// cluster per vector runs the whole TLM (mode kModeTlm, steps k0..k1-1, with
-// the observation gathers y = R^{-1/2} O x at interval ends when y != null) or
-// ADJ sweep (kModeAdj, with the scatters) with the RK state in shared memory.
-bool bve_cluster_ok(int n, int nvec);
-void bve_cluster_sweep(int n, int mode, double* state, int nvec, const double* base_w, const double* base_p, int k0,
-                       int k1, const long long* idx, int n_obs, int spi, const double* w, double* y, long long m,
-                       const double4* tab, double dt, double nu, double js, double ls, cudaStream_t st);
-
 void gather_obs(const double* f, long long dim, const long long* idx, int n_obs, const double* w, double* y,
                 long long m, int nvec, cudaStream_t st);
 void scatter_obs(double* f, long long dim, const long long* idx, int n_obs, const double* w, const double* y,

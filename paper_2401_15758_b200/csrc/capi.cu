@@ -1,6 +1,7 @@
 // extern "C" boundary (include/sdv.h). Converts C++ exceptions into status
 // codes + a thread-local message, never throwing across the ABI.
 #include <cstring>
+#include <mutex>
 #include <limits>
 #include <string>
 
@@ -8,8 +9,20 @@
 #include "engine.hpp"
 #include "solver.hpp"
 
+// Scratch device buffers for the host-pointer entry points.
+struct Scratch {
+  sdv::DevBuf<double> a, b;
+};
+// One problem = one CUDA stream + its workspaces. Calls on one problem (and on
+// its trajectories) are serialised by `mu`, so the reference's concurrent
+// callers (apply_columns worker threads on one trajectory,
+// proj/src/sketch.cpp:129-139; "safe to call concurrently",
+// proj/include/sketchdav/model.hpp:9-13) are safe; distinct problems share no
+// mutable state and run concurrently on their own streams.
 struct sdv_problem {
   std::unique_ptr<sdv::Problem> p;
+  mutable std::mutex mu;
+  Scratch sc;
 };
 struct sdv_traj {
   sdv_problem* owner = nullptr;
@@ -40,14 +53,7 @@ void need(const void* p, const char* what) {
   if (!p) throw std::invalid_argument(std::string("null argument: ") + what);
 }
 
-// Scratch device buffers for the host-pointer entry points.
-struct Scratch {
-  sdv::DevBuf<double> a, b;
-};
-Scratch& scratch() {
-  static Scratch s;
-  return s;
-}
+using Lock = std::lock_guard<std::mutex>;
 }  // namespace
 
 namespace {
@@ -56,8 +62,9 @@ int block_host(sdv_traj* t, const double* in, long long in_rows, int s, double* 
   return guard([&] {
     need(t, "trajectory");
     if (s < 1) throw std::invalid_argument("block: need s >= 1");
+    Lock lk(t->owner->mu);
     auto& q = *t->owner->p;
-    auto& sc = scratch();
+    auto& sc = t->owner->sc;
     sc.a.upload(in, static_cast<size_t>(in_rows) * s, q.stream());
     sc.b.ensure(static_cast<size_t>(out_rows) * s);
     f(q, sc.a.get(), sc.b.get());
@@ -71,7 +78,12 @@ extern "C" {
 
 const char* sdv_last_error(void) { return g_err.c_str(); }
 const char* sdv_version(void) { return "sdv-b200 0.1 (sm_100a)"; }
-unsigned long long sdv_launch_count(void) { return sdv::g_launches; }
+unsigned long long sdv_launch_count(void) { return sdv::g_launches.load(); }
+int sdv_path_counts(uint64_t* out, int n) {
+  for (int i = 0; i < n && i < sdv::kPathCount; ++i) out[i] = sdv::g_path[i].load();
+  return sdv::kPathCount;
+}
+const char* sdv_path_name(int i) { return sdv::path_name(i); }
 
 int sdv_device_init(int device) {
   return guard([&] {
@@ -119,6 +131,7 @@ void sdv_problem_destroy(sdv_problem* p) { delete p; }
 int sdv_problem_dims(const sdv_problem* p, int64_t dims[6]) {
   return guard([&] {
     need(p, "problem");
+    Lock lk(p->mu);
     const auto& q = *p->p;
     dims[0] = q.dim();
     dims[1] = q.m();
@@ -133,8 +146,9 @@ int sdv_forward(sdv_problem* p, const double* x0, int steps, double* out) {
   return guard([&] {
     need(p, "problem");
     if (steps < 0) throw std::invalid_argument("forward: steps must be >= 0");
+    Lock lk(p->mu);
     auto& q = *p->p;
-    auto& s = scratch();
+    auto& s = p->sc;
     s.a.upload(x0, static_cast<size_t>(q.dim()), q.stream());
     s.b.ensure(static_cast<size_t>(q.dim()));
     q.forward(s.a.get(), steps, s.b.get());
@@ -146,6 +160,7 @@ int sdv_forward(sdv_problem* p, const double* x0, int steps, double* out) {
 int sdv_linearize_dev(sdv_problem* p, const double* x0_dev, sdv_traj** out) {
   return guard([&] {
     need(p, "problem");
+    Lock lk(p->mu);
     need(out, "out");
     auto t = std::make_unique<sdv_traj>();
     t->owner = p;
@@ -156,6 +171,7 @@ int sdv_linearize_dev(sdv_problem* p, const double* x0_dev, sdv_traj** out) {
 int sdv_linearize(sdv_problem* p, const double* x0, sdv_traj** out) {
   return guard([&] {
     need(p, "problem");
+    Lock lk(p->mu);
     need(x0, "x0");
     auto& q = *p->p;
     sdv::DevBuf<double> d;
@@ -166,11 +182,16 @@ int sdv_linearize(sdv_problem* p, const double* x0, sdv_traj** out) {
     *out = t.release();
   });
 }
-void sdv_traj_destroy(sdv_traj* t) { delete t; }
+void sdv_traj_destroy(sdv_traj* t) {
+  if (!t) return;
+  Lock lk(t->owner->mu);
+  delete t;
+}
 
 int sdv_traj_state_at(const sdv_traj* t, int step, double* out) {
   return guard([&] {
     need(t, "trajectory");
+    Lock lk(t->owner->mu);
     auto& q = *t->owner->p;
     SDV_CUDA(cudaMemcpyAsync(out, t->t->state_at(step), sizeof(double) * q.dim(), cudaMemcpyDeviceToHost,
                              q.stream()));
@@ -198,8 +219,9 @@ int sdv_prior_sqrt_block(sdv_problem* p, const double* v, int s, double* out) {
   return guard([&] {
     need(p, "problem");
     if (s < 1) throw std::invalid_argument("block: need s >= 1");
+    Lock lk(p->mu);
     auto& q = *p->p;
-    auto& sc = scratch();
+    auto& sc = p->sc;
     sc.a.upload(v, static_cast<size_t>(q.dim()) * s, q.stream());
     sc.b.ensure(static_cast<size_t>(q.dim()) * s);
     q.prior_sqrt(sc.a.get(), sc.b.get(), s);
@@ -229,18 +251,21 @@ int sdv_gram_apply_block(sdv_traj* t, const double* V, int s, double* HV) {
 int sdv_misfit_apply_block_dev(sdv_traj* t, const double* V, int s, double* Y) {
   return guard([&] {
     need(t, "trajectory");
+    Lock lk(t->owner->mu);
     t->owner->p->misfit_apply(*t->t, V, s, Y);
   });
 }
 int sdv_misfit_adjoint_block_dev(sdv_traj* t, const double* W, int s, double* Z) {
   return guard([&] {
     need(t, "trajectory");
+    Lock lk(t->owner->mu);
     t->owner->p->misfit_adjoint(*t->t, W, s, Z);
   });
 }
 int sdv_gram_apply_block_dev(sdv_traj* t, const double* V, int s, double* HV) {
   return guard([&] {
     need(t, "trajectory");
+    Lock lk(t->owner->mu);
     t->owner->p->gram_apply(*t->t, V, s, HV);
   });
 }
@@ -249,6 +274,7 @@ int sdv_evaluate(sdv_problem* p, const double* x0, const double* z, double* cost
                  double* lambda0) {
   return guard([&] {
     need(p, "problem");
+    Lock lk(p->mu);
     need(x0, "x0");
     need(cost, "cost");
     auto& q = *p->p;
@@ -268,6 +294,7 @@ int sdv_woodbury_apply(sdv_problem* p, int64_t l, const double* basis, const dou
                        double* out) {
   return guard([&] {
     need(p, "problem");
+    Lock lk(p->mu);
     auto& q = *p->p;
     sdv::DeviceEVD e;
     e.upload(q.dim(), static_cast<int>(l), basis, eig, q.stream());
@@ -283,6 +310,7 @@ int sdv_woodbury_apply(sdv_problem* p, int64_t l, const double* basis, const dou
 int sdv_thin_qr(sdv_problem* p, int64_t n, int64_t l, const double* y, double* q, double* r, int* ndef) {
   return guard([&] {
     need(p, "problem");
+    Lock lk(p->mu);
     cudaStream_t st = p->p->stream();
     sdv::DevBuf<double> d;
     d.upload(y, static_cast<size_t>(n * l), st);
@@ -297,6 +325,7 @@ int sdv_sketch(sdv_traj* t, int method, int rank, int rank2, uint64_t seed, doub
                int64_t counts[3]) {
   return guard([&] {
     need(t, "trajectory");
+    Lock lk(t->owner->mu);
     need(eig, "eig");
     auto& q = *t->owner->p;
     sdv::MisfitOp op(q, *t->t);
@@ -315,6 +344,7 @@ int sdv_sketch(sdv_traj* t, int method, int rank, int rank2, uint64_t seed, doub
 int sdv_lanczos_sketch(sdv_traj* t, int rank, const double* start, double* eig, double* basis, int64_t counts[3]) {
   return guard([&] {
     need(t, "trajectory");
+    Lock lk(t->owner->mu);
     need(start, "start");
     need(eig, "eig");
     auto& q = *t->owner->p;
@@ -337,6 +367,7 @@ int sdv_sketch_adaptive(sdv_traj* t, int method, int rank, int growth, int max_r
                         uint64_t seed, double* eig, double* basis, int64_t counts[5], double* kappa, int max_kappa) {
   return guard([&] {
     need(t, "trajectory");
+    Lock lk(t->owner->mu);
     need(eig, "eig");
     need(counts, "counts");
     if (method < 0 || method > 2) throw std::invalid_argument("sdv_sketch_adaptive: method must be 0, 1 or 2");
@@ -371,6 +402,7 @@ int sdv_sketch_adaptive(sdv_traj* t, int method, int rank, int growth, int max_r
 int sdv_cond_estimate(sdv_traj* t, int64_t l, const double* basis, const double* eig, uint64_t seed, double* kappa) {
   return guard([&] {
     need(t, "trajectory");
+    Lock lk(t->owner->mu);
     need(kappa, "kappa");
     auto& q = *t->owner->p;
     sdv::DeviceEVD e;
@@ -384,6 +416,7 @@ int sdv_pcg_solve(sdv_traj* t, const double* rhs, int64_t l, const double* basis
                   int max_iter, double* x, int info[2]) {
   return guard([&] {
     need(t, "trajectory");
+    Lock lk(t->owner->mu);
     auto& q = *t->owner->p;
     const size_t n = static_cast<size_t>(q.dim());
     sdv::DeviceEVD e;
@@ -403,6 +436,7 @@ int sdv_gn_solve(sdv_problem* p, const sdv_gn_config* cfg, double* analysis, dou
                  double summary[5], double* eig0, int max_eig) {
   return guard([&] {
     need(p, "problem");
+    Lock lk(p->mu);
     need(cfg, "config");
     sdv::GNConfig g;
     g.mode = cfg->mode;
@@ -459,6 +493,7 @@ int sdv_memcpy_dtoh(void* dst, const void* src, size_t bytes) {
 int sdv_synchronize(sdv_problem* p) {
   return guard([&] {
     need(p, "problem");
+    Lock lk(p->mu);
     SDV_CUDA(cudaStreamSynchronize(p->p->stream()));
   });
 }
@@ -473,6 +508,7 @@ int sdv_event_destroy(void* ev) { return guard([&] { SDV_CUDA(cudaEventDestroy(s
 int sdv_event_record(sdv_problem* p, void* ev) {
   return guard([&] {
     need(p, "problem");
+    Lock lk(p->mu);
     SDV_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev), p->p->stream()));
   });
 }
@@ -485,6 +521,7 @@ int sdv_event_elapsed_ms(void* a, void* b, float* ms) {
 int sdv_probe_stage_kernels(sdv_traj* t, int s, int stages, float* ms_stage, float* ms_col) {
   return guard([&] {
     need(t, "trajectory");
+    Lock lk(t->owner->mu);
     t->owner->p->probe_stage_kernels(*t->t, s, stages, ms_stage, ms_col);
   });
 }

@@ -475,14 +475,7 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
     else
       burgers_tlm(a, state, nvec, st_);
     count_launch();
-    return;
-  }
-  if (bve_cluster_ok(d_.n, nvec)) {
-    const StageArgs b = bve_args(d_);
-    bve_cluster_sweep(d_.n, kModeTlm, state, nvec, tr.w.get(), tr.p.get(), k0, k1, idx_.get(), static_cast<int>(n_obs_),
-                      d_.spi, w, y, m(), reinterpret_cast<const double4*>(solve_tab_.get()), b.dt, b.nu, b.inv12h2,
-                      b.invh2, st_);
-    count_launch();
+    count_path(kPathBurgers);
     return;
   }
   ensure_work(nvec);
@@ -602,14 +595,7 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
     else
       burgers_adj(a, state, nvec, st_);
     count_launch();
-    return;
-  }
-  if (bve_cluster_ok(d_.n, nvec)) {
-    const StageArgs b = bve_args(d_);
-    bve_cluster_sweep(d_.n, kModeAdj, state, nvec, tr.w.get(), tr.p.get(), k0, k1, idx_.get(), static_cast<int>(n_obs_),
-                      d_.spi, w, const_cast<double*>(y), m(), reinterpret_cast<const double4*>(solve_tab_.get()), b.dt,
-                      b.nu, b.inv12h2, b.invh2, st_);
-    count_launch();
+    count_path(kPathBurgers);
     return;
   }
   ensure_work(nvec);
@@ -819,7 +805,7 @@ void Problem::gram_apply(const Trajectory& tr, const double* v, int s, double* h
     return;
   }
   cudaGraph_t graph = nullptr;
-  const unsigned long long before = g_launches;
+  const unsigned long long before = t_launches;
   SDV_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
   try {
     run();
@@ -829,8 +815,9 @@ void Problem::gram_apply(const Trajectory& tr, const double* v, int s, double* h
     throw;
   }
   SDV_CUDA(cudaStreamEndCapture(st_, &graph));
-  hit->nodes = g_launches - before;  // kernels per replay
-  g_launches = before;
+  hit->nodes = t_launches - before;  // kernels per replay (recorded, not launched)
+  g_launches.fetch_sub(hit->nodes, std::memory_order_relaxed);
+  t_launches = before;
   SDV_CUDA(cudaGraphInstantiate(&hit->exec, graph, 0));
   SDV_CUDA(cudaGraphDestroy(graph));
   SDV_CUDA(cudaGraphLaunch(hit->exec, st_));
@@ -847,8 +834,14 @@ Problem::~Problem() {
   clear_graphs();
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
-  if (st2_) cudaStreamDestroy(st2_);
-  if (st_) cudaStreamDestroy(st_);
+  if (st2_) {
+    release_stream_work(st2_);
+    cudaStreamDestroy(st2_);
+  }
+  if (st_) {
+    release_stream_work(st_);
+    cudaStreamDestroy(st_);
+  }
 }
 
 // --------------------------------------------- reference BVE (kModelBVE3) --

@@ -4,11 +4,48 @@
 #include "linalg_kernels.cuh"
 
 #include <cfloat>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <cmath>
 
 namespace sdv {
 
-unsigned long long g_launches = 0;
+std::atomic<unsigned long long> g_launches{0};
+
+// Per-stream device workspaces (a Problem owns its streams, so two problems
+// driven from two threads never share a buffer; work on one stream is
+// ordered, so reuse within a stream is safe).
+namespace {
+std::mutex g_work_mu;
+std::map<cudaStream_t, std::unique_ptr<StreamWork>>& work_registry() {
+  static auto* reg = new std::map<cudaStream_t, std::unique_ptr<StreamWork>>();  // outlives static dtors
+  return *reg;
+}
+}  // namespace
+StreamWork& stream_work(cudaStream_t st) {
+  std::lock_guard<std::mutex> l(g_work_mu);
+  auto& w = work_registry()[st];
+  if (!w) w = std::make_unique<StreamWork>();
+  return *w;
+}
+void release_stream_work(cudaStream_t st) {
+  std::unique_ptr<StreamWork> dead;
+  {
+    std::lock_guard<std::mutex> l(g_work_mu);
+    auto it = work_registry().find(st);
+    if (it == work_registry().end()) return;
+    dead = std::move(it->second);
+    work_registry().erase(it);
+  }
+}
+thread_local unsigned long long t_launches = 0;
+std::atomic<unsigned long long> g_path[kPathCount];
+const char* path_name(int p) {
+  static const char* const names[kPathCount] = {"bve_stage_fused", "bve_carry",     "bve_stage_lite", "bve_stage_plain",
+                                                "bve_col_solve",   "bve_col_fft",   "burgers_sweep"};
+  return p >= 0 && p < kPathCount ? names[p] : nullptr;
+}
 
 namespace {
 constexpr int kRedBlocks = 296;  // 2 CTAs per SM on 148 SMs
@@ -56,8 +93,8 @@ __global__ void __launch_bounds__(kRedThreads) sum_partials_kernel(const double*
   (void)ncols;
 }
 
-DevBuf<double>& partial_buf(size_t n) {
-  static DevBuf<double> buf;
+DevBuf<double>& partial_buf(size_t n, cudaStream_t st) {
+  DevBuf<double>& buf = stream_work(st).partial;
   buf.ensure(n);
   return buf;
 }
@@ -275,7 +312,7 @@ int grid_for(long long n, int th = 256) {
 }  // namespace
 
 void dev_dot(const double* a, const double* b, long long n, double* out, cudaStream_t st) {
-  DevBuf<double>& part = partial_buf(kRedBlocks);
+  DevBuf<double>& part = partial_buf(kRedBlocks, st);
   dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(a, b, n, part.get());
   sum_partials_kernel<<<1, kRedThreads, 0, st>>>(part.get(), kRedBlocks, 1, out);
   count_launch(2);
@@ -286,7 +323,7 @@ void dev_coldots(const double* a, long long lda, const double* b, long long ldb,
                  cudaStream_t st) {
   if (ncols <= 0) return;
   const int nchunks = static_cast<int>(std::min<long long>(64, std::max<long long>(1, n / 4096)));
-  DevBuf<double>& part = partial_buf(static_cast<size_t>(nchunks) * ncols);
+  DevBuf<double>& part = partial_buf(static_cast<size_t>(nchunks) * ncols, st);
   coldot_partial_kernel<<<dim3(nchunks, ncols), kRedThreads, 0, st>>>(a, lda, b, ldb, n, nchunks, part.get());
   sum_partials_kernel<<<ncols, kRedThreads, 0, st>>>(part.get(), nchunks, ncols, out);
   count_launch(2);
@@ -311,7 +348,7 @@ void dev_gemm_tn(long long n, int k, int l, const double* a, const double* b, do
   if (k <= 0 || l <= 0) return;
   const int tk = (k + kGT - 1) / kGT, tl = (l + kGT - 1) / kGT;
   int nchunks = static_cast<int>(std::max<long long>(1, std::min<long long>((n + 4095) / 4096, 592 / (tk * tl) + 1)));
-  DevBuf<double>& part = partial_buf(static_cast<size_t>(nchunks) * k * l);
+  DevBuf<double>& part = partial_buf(static_cast<size_t>(nchunks) * k * l, st);
   gemm_tn_partial_kernel<<<dim3(nchunks, tk, tl), 256, 0, st>>>(n, k, l, a, b, nchunks, part.get());
   sum_partials_kernel<<<k * l, kRedThreads, 0, st>>>(part.get(), nchunks, k * l, c);
   count_launch(2);
@@ -347,9 +384,13 @@ void dev_trsm_rows_lower(long long n, int l, const double* lmat, const double* y
 
 int dev_householder_qr(long long n, int l, double* y, double* r_host, cudaStream_t st) {
   if (n < l) throw std::invalid_argument("thin_qr: need rows >= cols");
-  static DevBuf<House> hs;
-  static DevBuf<double> w, scal, qbuf, sgn;
-  hs.ensure(static_cast<size_t>(l));
+  StreamWork& ws = stream_work(st);
+  DevBuf<double>& hs = ws.qr_house;  // House records (3 doubles each)
+  DevBuf<double>& w = ws.qr_w;
+  DevBuf<double>& scal = ws.qr_scal;
+  DevBuf<double>& qbuf = ws.qr_q;
+  DevBuf<double>& sgn = ws.qr_sgn;
+  hs.ensure(static_cast<size_t>(3) * l);
   w.ensure(static_cast<size_t>(l));
   scal.ensure(2);
   qbuf.ensure(static_cast<size_t>(n) * l);
@@ -360,14 +401,14 @@ int dev_householder_qr(long long n, int l, double* y, double* r_host, cudaStream
     // tail norm^2 and c0
     sumsq_tail_partial_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, j, y, part.get());
     sum_partials_kernel<<<1, kRedThreads, 0, st>>>(part.get(), kRedBlocks, 1, scal.get() + 1);
-    house_scalar_kernel<<<1, 1, 0, st>>>(y + j + static_cast<long long>(j) * n, scal.get() + 1, hs.get() + j);
-    house_scale_kernel<<<grid_for(n - j), 256, 0, st>>>(n, j, y, hs.get() + j);
+    house_scalar_kernel<<<1, 1, 0, st>>>(y + j + static_cast<long long>(j) * n, scal.get() + 1, reinterpret_cast<House*>(hs.get()) + j);
+    house_scale_kernel<<<grid_for(n - j), 256, 0, st>>>(n, j, y, reinterpret_cast<House*>(hs.get()) + j);
     count_launch(4);
     const int nc = l - j - 1;
     if (nc > 0) {
       const double* v = y + static_cast<long long>(j) * n;
       house_dot_partial_kernel<<<dim3(nchunks, nc), kRedThreads, 0, st>>>(n, j, v, y, j + 1, nchunks, part.get());
-      house_dot_final_kernel<<<nc, kRedThreads, 0, st>>>(j, n, y, j + 1, nchunks, part.get(), hs.get() + j, w.get());
+      house_dot_final_kernel<<<nc, kRedThreads, 0, st>>>(j, n, y, j + 1, nchunks, part.get(), reinterpret_cast<House*>(hs.get()) + j, w.get());
       house_update_kernel<<<dim3(grid_for(n - j) / 4 + 1, nc), 256, 0, st>>>(n, j, v, y, j + 1, nc, w.get());
       count_launch(3);
     }
@@ -385,7 +426,7 @@ int dev_householder_qr(long long n, int l, double* y, double* r_host, cudaStream
     const double* v = y + static_cast<long long>(j) * n;
     const int nc = l - j;
     house_dot_partial_kernel<<<dim3(nchunks, nc), kRedThreads, 0, st>>>(n, j, v, q, j, nchunks, part.get());
-    house_dot_final_kernel<<<nc, kRedThreads, 0, st>>>(j, n, q, j, nchunks, part.get(), hs.get() + j, w.get());
+    house_dot_final_kernel<<<nc, kRedThreads, 0, st>>>(j, n, q, j, nchunks, part.get(), reinterpret_cast<House*>(hs.get()) + j, w.get());
     house_update_kernel<<<dim3(grid_for(n - j) / 4 + 1, nc), 256, 0, st>>>(n, j, v, q, j, nc, w.get());
     count_launch(3);
   }

@@ -2,13 +2,46 @@
 // All reductions are deterministic (fixed grid, fixed-order tree).
 #pragma once
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace sdv {
 
-// Number of kernel launches issued by this library (for bench gpu_launches).
-extern unsigned long long g_launches;
-inline void count_launch(unsigned long long k = 1) { g_launches += k; }
+// Number of kernel launches issued by this library (for bench gpu_launches),
+// process-wide (atomic) and per calling thread (graph capture subtracts the
+// launches it only recorded, without racing other threads' counts).
+extern std::atomic<unsigned long long> g_launches;
+extern thread_local unsigned long long t_launches;
+inline void count_launch(unsigned long long k = 1) {
+  g_launches.fetch_add(k, std::memory_order_relaxed);
+  t_launches += k;
+}
+
+// Which kernel variant the sweeps took (sdv_path_counts): one count per
+// host-side launch decision (a CUDA-graph replay is counted once, at capture).
+enum KernelPath {
+  kPathBveStageFused = 0,  // stage_kernel<N, TLM/ADJ, 8, stage, fused> (the hot path)
+  kPathBveCarry,           // carry_kernel<N> (tile carries of the fused Poisson path)
+  kPathBveStageLite,       // fused kernel as a plain stage on 2-row tiles (small blocks)
+  kPathBveStagePlain,      // unfused stage_kernel (8- or 2-row tiles, NL forward)
+  kPathBveColSolve,        // col_solve_kernel (recurrence column pass)
+  kPathBveColFft,          // col_kernel (y-FFT column pass)
+  kPathBurgers,            // whole-sweep Burgers kernels
+  kPathCount
+};
+extern std::atomic<unsigned long long> g_path[kPathCount];
+inline void count_path(int p, unsigned long long k = 1) { g_path[p].fetch_add(k, std::memory_order_relaxed); }
+const char* path_name(int p);
+
+// Device workspaces owned by one CUDA stream (reduction partials, QR
+// scratch, a host-readable dot result). Thread-safe lookup; released when the
+// owning Problem destroys the stream.
+struct StreamWork {
+  DevBuf<double> partial, qr_house, qr_w, qr_scal, qr_q, qr_sgn, dot;
+};
+StreamWork& stream_work(cudaStream_t st);
+void release_stream_work(cudaStream_t st);
 
 // out[0] = sum_i a[i] * b[i] (device scalar), deterministic.
 void dev_dot(const double* a, const double* b, long long n, double* out, cudaStream_t st);

@@ -29,7 +29,8 @@ __global__ void mul_elem_kernel(int l, const double* __restrict__ c, double* __r
 }
 
 double host_dot(const double* a, const double* b, long long n, cudaStream_t st) {
-  static DevBuf<double> r(1);
+  DevBuf<double>& r = stream_work(st).dot;
+  r.ensure(1);
   dev_dot(a, b, n, r.get(), st);
   double h = 0;
   SDV_CUDA(cudaMemcpyAsync(&h, r.get(), sizeof(double), cudaMemcpyDeviceToHost, st));

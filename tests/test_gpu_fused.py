@@ -1,56 +1,149 @@
 """GPU parity of the fused Poisson path (stage kernels with tile-local
-y-recurrences + the tile-carry pass, bve_carry), taken by block sweeps wide
-enough for 8-row stage tiles. Blocks here are sized to take that path; the
-same products through the column-pass path (SDV_NO_FUSE=1) and the CPU
-oracle are the references. Tolerances as test_gpu_parity (1e-10 relative
-for Hessian products, dot test 1e-10).
+y-recurrences + the tile-carry pass, bve_carry): the C3 hot path.
+
+A block is split into two sweep lanes of ceil(s/2) and floor(s/2) vectors
+(engine.cu split_lanes), and a lane takes the fused path only when its 8-row
+tiles fill >= 2 CTAs per SM: (n/8) * lane >= 296, i.e. lanes of >= 5 / 10 /
+19 / 37 vectors at 512^2 / 256^2 / 128^2 / 64^2, so blocks of >= 10 / 20 /
+38 / 74 vectors. Every case below is sized for that and ASSERTS the kernel
+path it took through the per-variant launch counters (sdv_path_counts). The
+references are the column-pass path (SDV_NO_FUSE=1 SDV_NO_LITE=1: unfused
+8-row stage kernels + col_solve_kernel, also asserted) and the CPU oracle.
+Tolerances as test_gpu_parity (1e-10 relative for Hessian products and the
+dot test, 1e-8 for sketch eigenvalues).
 """
 import os
 
 import numpy as np
 import pytest
 
-from test_gpu_parity import pair, rel
+from test_gpu_parity import eig_rel, pair, rel
 
 pytestmark = pytest.mark.gpu
 
-# (config, steps, spi, s): s is the smallest block that takes the fused path
-# at that grid (8-row tiles fill >= 2 CTAs per SM), plus one wider block.
-CASES = [(3, 16, 8, 5), (3, 8, 4, 12), (2, 40, -1, 19), (4, 40, -1, 10), (4, 20, 10, 23)]
+# smallest block width that puts BOTH lanes on the fused path, per grid size
+FUSED_MIN = {64: 74, 128: 38, 256: 20, 512: 10}
+
+# (config, steps, spi, s): the minimum fused width and wider/odd widths
+CASES = [(3, 16, 8, 10), (3, 8, 4, 13), (2, 40, -1, 38), (2, 20, 10, 41), (4, 40, -1, 20), (4, 20, 10, 23)]
 
 
-def _no_fuse(flag):
-    if flag:
-        os.environ["SDV_NO_FUSE"] = "1"
+def _env(column_path):
+    for k in ("SDV_NO_FUSE", "SDV_NO_LITE"):
+        if column_path:
+            os.environ[k] = "1"
+        else:
+            os.environ.pop(k, None)
+
+
+def run_paths(sdv, fn, column_path):
+    """fn() under the fused (default) or column-pass path; returns (result, path deltas) and asserts the path."""
+    _env(column_path)
+    try:
+        before = sdv.path_counts()
+        out = fn()
+        took = sdv.path_delta(before)
+    finally:
+        _env(False)
+    if column_path:
+        assert took["bve_stage_fused"] == 0 and took["bve_stage_lite"] == 0 and took["bve_carry"] == 0, took
+        assert took["bve_stage_plain"] > 0 and took["bve_col_solve"] > 0, took
     else:
-        os.environ.pop("SDV_NO_FUSE", None)
+        assert took["bve_stage_fused"] > 0 and took["bve_carry"] > 0, took
+        assert took["bve_stage_lite"] == 0 and took["bve_stage_plain"] == 0, took
+    return out, took
+
+
+def test_fused_min_width_table(sdv):
+    """The widths above are the boundary: one vector fewer leaves a lane off the fused path."""
+    from paper_2401_15758_b200 import api, scenario
+
+    for n, s in FUSED_MIN.items():
+        spec = scenario.ConfigSpec(**{**scenario.CONFIGS[2].__dict__, "name": f"bve-{n}", "n": n, "steps": 2,
+                                      "spi": 1, "dt": 0.01 * 128 / n})
+        sc = scenario.build(spec)
+        tr = sc.problem.linearize(sc.problem.background)
+        for width, fused_lanes in ((s, 2), (s - 1, 1)):
+            V = api.gaussian_matrix(sc.problem.n, width, 3)
+            before = sdv.path_counts()
+            tr.misfit_apply(V)
+            d = sdv.path_delta(before)
+            # TLM over 2 RK4 steps: 8 stage launches per lane
+            assert d["bve_stage_fused"] == 8 * fused_lanes, (n, width, d)
 
 
 @pytest.mark.parametrize("cfg,steps,spi,s", CASES)
 def test_fused_gram_matches_column_path_and_oracle(oracle, sdv, cfg, steps, spi, s):
     osc, prob = pair(oracle, cfg, steps, spi)
+    assert s >= FUSED_MIN[osc_n(osc)]
     otr = osc.linearize(osc.background)
     gtr = prob.linearize(osc.background)
     V = oracle.gaussian_matrix(osc.n, s, 31)
     W = oracle.gaussian_matrix(osc.m, s, 32)
-    try:
-        _no_fuse(False)
-        HV, Y, Z = gtr.gram(V), gtr.misfit_apply(V), gtr.misfit_adjoint(W)
-        _no_fuse(True)
-        HV0, Y0, Z0 = gtr.gram(V), gtr.misfit_apply(V), gtr.misfit_adjoint(W)
-    finally:
-        _no_fuse(False)
+    (HV, Y, Z), _ = run_paths(sdv, lambda: (gtr.gram(V), gtr.misfit_apply(V), gtr.misfit_adjoint(W)), False)
+    (HV0, Y0, Z0), _ = run_paths(sdv, lambda: (gtr.gram(V), gtr.misfit_apply(V), gtr.misfit_adjoint(W)), True)
     for j in range(s):
         assert rel(HV[j], HV0[j]) <= 1e-12, ("HV vs column path", j)
         assert rel(Y[j], Y0[j]) <= 1e-12, ("Y vs column path", j)
         assert rel(Z[j], Z0[j]) <= 1e-12, ("Z vs column path", j)
         assert abs(Y[j] @ W[j] - V[j] @ Z[j]) <= 1e-10 * np.linalg.norm(V[j]) * np.linalg.norm(W[j])
-    # oracle on the first and last columns (1e-10 relative)
-    for j in (0, s - 1):
-        Yo = otr.misfit_apply(V[j:j + 1], workers=8)
-        assert rel(Y[j], Yo[0]) <= 1e-10, ("Y vs oracle", j)
-        assert rel(HV[j], otr.misfit_adjoint(Yo)[0]) <= 1e-10, ("HV vs oracle", j)
-        assert rel(Z[j], otr.misfit_adjoint(W[j:j + 1], workers=8)[0]) <= 1e-10, ("Z vs oracle", j)
+    # oracle on the first and last column of each lane (1e-10 relative)
+    a = (s + 1) // 2
+    cols = [0, a - 1, a, s - 1]
+    Yo = otr.misfit_apply(V[cols], workers=len(cols))
+    HVo = otr.misfit_adjoint(Yo, workers=len(cols))
+    Zo = otr.misfit_adjoint(W[cols], workers=len(cols))
+    for i, j in enumerate(cols):
+        assert rel(Y[j], Yo[i]) <= 1e-10, ("Y vs oracle", j)
+        assert rel(HV[j], HVo[i]) <= 1e-10, ("HV vs oracle", j)
+        assert rel(Z[j], Zo[i]) <= 1e-10, ("Z vs oracle", j)
+
+
+def osc_n(osc):
+    return int(round(np.sqrt(osc.n)))
+
+
+def test_c3_bench_width_parity(oracle, sdv):
+    """C3 at the benchmarked block width s = 110 (two fused lanes of 55, the exact launch shape bench.py
+    times), on an 8-step window (2 observation intervals): the first and last column of each lane vs the
+    oracle <= 1e-10 for A V, A^T (A V) and A^T W, and the dot test on every column."""
+    osc, prob = pair(oracle, 3, 8, 4)
+    otr = osc.linearize(osc.background)
+    gtr = prob.linearize(osc.background)
+    s = 110
+    V = oracle.gaussian_matrix(osc.n, s, 71)
+    W = oracle.gaussian_matrix(osc.m, s, 72)
+    (HV, Y, Z), took = run_paths(sdv, lambda: (gtr.gram(V), gtr.misfit_apply(V), gtr.misfit_adjoint(W)), False)
+    # 8 steps x 4 stages per sweep; gram = TLM + ADJ; 2 lanes; gram + apply + adjoint
+    assert took["bve_stage_fused"] == 2 * (2 * 32 + 32 + 32 + 2), took
+    for j in range(s):
+        assert abs(Y[j] @ W[j] - V[j] @ Z[j]) <= 1e-10 * np.linalg.norm(V[j]) * np.linalg.norm(W[j]), j
+    cols = [0, 54, 55, 109]
+    Yo = otr.misfit_apply(V[cols], workers=4)
+    HVo = otr.misfit_adjoint(Yo, workers=4)
+    Zo = otr.misfit_adjoint(W[cols], workers=4)
+    for i, j in enumerate(cols):
+        assert rel(Y[j], Yo[i]) <= 1e-10, ("Y", j)
+        assert rel(HV[j], HVo[i]) <= 1e-10, ("HV", j)
+        assert rel(Z[j], Zo[i]) <= 1e-10, ("Z", j)
+
+
+def test_c3_randsvd_k100_eigenvalues(oracle, sdv):
+    """C3's own sketch, RandSVD with k = 100, p = 10 (one block of l = 110 TLM + 110 ADJ sweeps on the fused
+    path) on a 4-step window, seeded as gn_solve's first iteration (mix_seed(2, kIterSketchStream)):
+    eigenvalues within 1e-8 relative of the oracle's, orthonormal basis, identical apply counts
+    (proj/src/sketch.cpp:142-160)."""
+    osc, prob = pair(oracle, 3, 4, 2)
+    otr = osc.linearize(osc.background)
+    gtr = prob.linearize(osc.background)
+    seed = oracle.mix_seed(2, 0x736b6574636800)
+    (eg, bg, cg), _ = run_paths(sdv, lambda: gtr.sketch(0, 110, seed), False)
+    eo, bo, co = otr.sketch(0, 110, seed, workers=max(2, os.cpu_count() or 2))
+    assert tuple(cg) == tuple(co) == (110, 110, 110)
+    assert eig_rel(eg, eo) <= 1e-8
+    # the leading eigenvalues (the ones a k = 100 preconditioner keeps) individually
+    assert np.all(np.abs(eg[:100] - eo[:100]) <= 1e-8 * np.abs(eo[:100]) + 1e-12 * eo[0])
+    assert np.linalg.norm(bg @ bg.T - np.eye(110)) <= 1e-8
 
 
 def test_fused_sub_range_tlm_adj(oracle, sdv):
@@ -58,77 +151,49 @@ def test_fused_sub_range_tlm_adj(oracle, sdv):
     osc, prob = pair(oracle, 3, 8, 4)
     otr = osc.linearize(osc.background)
     gtr = prob.linearize(osc.background)
-    X = oracle.gaussian_matrix(osc.n, 6, 5)
+    X = oracle.gaussian_matrix(osc.n, 12, 5)
     for b, e in [(0, 8), (3, 7), (5, 6)]:
-        Tg, Ag = gtr.tlm_range(b, e, X), gtr.adj_range(b, e, X)
-        for j in (0, 5):
+        (Tg, Ag), _ = run_paths(sdv, lambda: (gtr.tlm_range(b, e, X), gtr.adj_range(b, e, X)), False)
+        for j in (0, 5, 6, 11):
             assert rel(Tg[j], otr.tlm_range(b, e, X[j])) <= 1e-10, (b, e, j)
             assert rel(Ag[j], otr.adj_range(b, e, X[j])) <= 1e-10, (b, e, j)
 
 
-@pytest.mark.parametrize("cfg,steps,spi,s", [(2, 40, -1, 1), (2, 20, 10, 3), (4, 20, 10, 1), (4, 40, -1, 4)])
-def test_cluster_sweeps_match_block_path_and_oracle(oracle, sdv, cfg, steps, spi, s):
-    """Cluster-resident small-block sweeps (bve_cluster.cu, opt-in SDV_CLUSTER)
-    vs the block path and the oracle: misfit apply/adjoint and Gram products."""
-    osc, prob = pair(oracle, cfg, steps, spi)
-    otr = osc.linearize(osc.background)
-    gtr = prob.linearize(osc.background)
-    V = oracle.gaussian_matrix(osc.n, s, 41)
-    W = oracle.gaussian_matrix(osc.m, s, 42)
-    try:
-        os.environ["SDV_CLUSTER"] = "8"
-        HV, Y, Z = gtr.gram(V), gtr.misfit_apply(V), gtr.misfit_adjoint(W)
-        os.environ.pop("SDV_CLUSTER", None)
-        HV0, Y0, Z0 = gtr.gram(V), gtr.misfit_apply(V), gtr.misfit_adjoint(W)
-    finally:
-        os.environ.pop("SDV_CLUSTER", None)
-    for j in range(s):
-        assert rel(HV[j], HV0[j]) <= 1e-12, ("HV vs block path", j)
-        assert rel(Y[j], Y0[j]) <= 1e-12, ("Y vs block path", j)
-        assert rel(Z[j], Z0[j]) <= 1e-12, ("Z vs block path", j)
-        assert abs(Y[j] @ W[j] - V[j] @ Z[j]) <= 1e-10 * np.linalg.norm(V[j]) * np.linalg.norm(W[j])
-    Yo = otr.misfit_apply(V[:1], workers=8)
-    assert rel(Y[0], Yo[0]) <= 1e-10
-    assert rel(HV[0], otr.misfit_adjoint(Yo)[0]) <= 1e-10
-    assert rel(Z[0], otr.misfit_adjoint(W[:1], workers=8)[0]) <= 1e-10
+def _grid_problem(n, steps, spi):
+    from paper_2401_15758_b200 import scenario
+
+    spec = scenario.ConfigSpec(**{**scenario.CONFIGS[2].__dict__, "name": f"bve-{n}", "n": n, "steps": steps,
+                                  "spi": spi, "dt": 0.01 * 128 / n})
+    sc = scenario.build(spec)
+    return sc.problem, sc.problem.linearize(sc.problem.background)
 
 
-@pytest.mark.parametrize("n,s", [(64, 37), (64, 40), (128, 21), (256, 11), (512, 7)])
+@pytest.mark.parametrize("n,s", [(64, 74), (64, 80), (128, 38), (128, 41), (256, 20), (256, 23), (512, 10),
+                                 (512, 13)])
 def test_fused_vs_column_path_other_grids(sdv, n, s):
     """Fused path on grids without an oracle case (64^2) and on odd block widths
     (two unequal sweep lanes): Gram products equal the column-pass path to 1e-12
     and the misfit pair passes the dot test."""
-    from paper_2401_15758_b200 import api, scenario
+    from paper_2401_15758_b200 import api
 
-    spec = scenario.ConfigSpec(**{**scenario.CONFIGS[2].__dict__, "name": f"bve-{n}", "n": n, "steps": 8, "spi": 4,
-                                  "dt": 0.01 * 128 / n})
-    sc = scenario.build(spec)
-    tr = sc.problem.linearize(sc.problem.background)
-    V = api.gaussian_matrix(sc.problem.n, s, 51)
-    W = api.gaussian_matrix(sc.problem.m, s, 52)
-    try:
-        _no_fuse(False)
-        HV, Y, Z = tr.gram(V), tr.misfit_apply(V), tr.misfit_adjoint(W)
-        _no_fuse(True)
-        HV0 = tr.gram(V)
-    finally:
-        _no_fuse(False)
+    prob, tr = _grid_problem(n, 8, 4)
+    V = api.gaussian_matrix(prob.n, s, 51)
+    W = api.gaussian_matrix(prob.m, s, 52)
+    (HV, Y, Z), _ = run_paths(sdv, lambda: (tr.gram(V), tr.misfit_apply(V), tr.misfit_adjoint(W)), False)
+    HV0, _ = run_paths(sdv, lambda: tr.gram(V), True)
     for j in range(s):
         assert rel(HV[j], HV0[j]) <= 1e-12, j
         assert abs(Y[j] @ W[j] - V[j] @ Z[j]) <= 1e-10 * np.linalg.norm(V[j]) * np.linalg.norm(W[j])
 
 
-@pytest.mark.parametrize("n,s", [(64, 37), (256, 12), (512, 5)])
+@pytest.mark.parametrize("n,s", [(64, 74), (256, 20), (512, 10)])
 def test_fused_sweeps_bitwise_deterministic(sdv, n, s):
     """Repeated fused-path Gram sweeps are bitwise identical (no shared-memory
     races in the in-place FFTs / per-team barriers, deterministic reductions)."""
-    from paper_2401_15758_b200 import api, scenario
+    from paper_2401_15758_b200 import api
 
-    spec = scenario.ConfigSpec(**{**scenario.CONFIGS[2].__dict__, "name": f"bve-{n}", "n": n, "steps": 4, "spi": 2,
-                                  "dt": 0.01 * 128 / n})
-    sc = scenario.build(spec)
-    tr = sc.problem.linearize(sc.problem.background)
-    V = api.gaussian_matrix(sc.problem.n, s, 61)
-    first = tr.gram(V)
+    prob, tr = _grid_problem(n, 4, 2)
+    V = api.gaussian_matrix(prob.n, s, 61)
+    first, _ = run_paths(sdv, lambda: tr.gram(V), False)
     for _ in range(3):
         assert np.array_equal(tr.gram(V), first)

@@ -177,3 +177,23 @@ def test_oracle_gn_c0_runs_and_decreases_cost(oracle):
     err_a = np.linalg.norm(r["analysis"] - sc.truth0)
     err_b = np.linalg.norm(sc.background - sc.truth0)
     assert err_a < 0.1 * err_b
+
+
+def test_oracle_threading_bitwise_neutral(oracle, tmp_path):
+    """ORACLE_THREADS (intra-operator par_for, oracle/src/dense.cpp) never changes a bit: the golden
+    fixtures made with it (tests/golden/make_golden.py) equal a serial oracle's results."""
+    import subprocess
+    import sys
+
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import oracle_lib as o; "
+            "sc = o.Scenario(2, steps=8, spi=4); tr = sc.linearize(sc.background); "
+            "np.save(%r, np.concatenate([tr.gram(o.gaussian_matrix(sc.n, 2, 3))[0], "
+            "sc.gn_solve(max_gn_iters=1, workers=2)['analysis']]))")
+    outs = []
+    for th in ("1", "4"):
+        f = str(tmp_path / f"o{th}.npy")
+        env = dict(os.environ, ORACLE_THREADS=th)
+        subprocess.run([sys.executable, "-c", code % (os.path.dirname(os.path.abspath(__file__)), f)], check=True,
+                       env=env)
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
