@@ -143,6 +143,15 @@ int sdv_woodbury_apply(sdv_problem* p, int64_t l, const double* basis, const dou
  * q (n x l), r (l x l); returns the deficient-column count in *ndef. */
 int sdv_thin_qr(sdv_problem* p, int64_t n, int64_t l, const double* y, double* q, double* r, int* ndef);
 
+/* Device-buffer forms for the sharded sketch: thin QR of a
+ * device block in place (y_dev n x l -> Q, r host l x l), and the RandSVD /
+ * Nystrom tail evd_from_gram_factor (proj/src/sketch.cpp:27-33, :191-197):
+ * from the tall factor Wt (n x l, device, unchanged) the basis Q_W U (device
+ * n x l, may be NULL) and eigenvalues S^2 - shift (floored at 0 if floor0). */
+int sdv_thin_qr_dev(sdv_problem* p, int64_t n, int64_t l, double* y_dev, double* r, int* ndef);
+int sdv_evd_from_tall_dev(sdv_problem* p, int64_t n, int64_t l, double* wt_dev, double shift, int floor0,
+                          double* basis_dev, double* eig);
+
 /* Sketch of the misfit Hessian at trajectory t (randsvd_sketch,
  * nystrom_sketch, singleview_sketch, lanczos_sketch; proj/src/sketch.cpp).
  * eig: rank values; basis: n x rank (may be NULL);

@@ -321,6 +321,39 @@ int sdv_thin_qr(sdv_problem* p, int64_t n, int64_t l, const double* y, double* q
   });
 }
 
+int sdv_thin_qr_dev(sdv_problem* p, int64_t n, int64_t l, double* y_dev, double* r, int* ndef) {
+  return guard([&] {
+    need(p, "problem");
+    need(y_dev, "y");
+    need(r, "r");
+    Lock lk(p->mu);
+    cudaStream_t st = p->p->stream();
+    const int nd = sdv::dev_householder_qr(n, static_cast<int>(l), y_dev, r, st);
+    SDV_CUDA(cudaStreamSynchronize(st));
+    if (ndef) *ndef = nd;
+  });
+}
+
+int sdv_evd_from_tall_dev(sdv_problem* p, int64_t n, int64_t l, double* wt_dev, double shift, int floor0,
+                          double* basis_dev, double* eig) {
+  return guard([&] {
+    need(p, "problem");
+    need(wt_dev, "wt");
+    need(eig, "eig");
+    if (n < 1 || l < 1 || l > n) throw std::invalid_argument("evd_from_tall: need 1 <= l <= n");
+    Lock lk(p->mu);
+    cudaStream_t st = p->p->stream();
+    const size_t nl = static_cast<size_t>(n) * static_cast<size_t>(l);
+    sdv::DevBuf<double> wt(nl);
+    SDV_CUDA(cudaMemcpyAsync(wt.get(), wt_dev, sizeof(double) * nl, cudaMemcpyDeviceToDevice, st));
+    sdv::DeviceEVD e = sdv::evd_from_tall(wt, n, static_cast<int>(l), shift, floor0 != 0, st);
+    if (basis_dev)
+      SDV_CUDA(cudaMemcpyAsync(basis_dev, e.basis.get(), sizeof(double) * nl, cudaMemcpyDeviceToDevice, st));
+    SDV_CUDA(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < l; ++i) eig[i] = e.eig[static_cast<size_t>(i)];
+  });
+}
+
 int sdv_sketch(sdv_traj* t, int method, int rank, int rank2, uint64_t seed, double* eig, double* basis,
                int64_t counts[3]) {
   return guard([&] {

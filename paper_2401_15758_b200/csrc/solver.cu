@@ -67,6 +67,8 @@ void copy_dev(double* dst, const double* src, long long n, cudaStream_t st) {
   SDV_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
 }
 
+}  // namespace
+
 // EVD of G^T G from a tall factor Wt (= G^T, n x l): Wt = Q R, R = U S V^T
 // => basis = Q U, eigenvalues = S^2 - shift (floored at 0 when shift > 0).
 // proj/src/sketch.cpp:27-33 (and the Nystrom tail, :191-197).
@@ -86,6 +88,7 @@ DeviceEVD evd_from_tall(DevBuf<double>& wt, long long n, int l, double shift, bo
   return e;
 }
 
+namespace {
 std::vector<double> col_norms(const double* y, long long n, int l, cudaStream_t st) {
   DevBuf<double> d(static_cast<size_t>(l));
   dev_coldots(y, n, y, n, n, l, d.get(), st);

@@ -23,6 +23,10 @@ struct DeviceEVD {
   void upload(long long n_, int l_, const double* basis_host, const double* eig_host, cudaStream_t st);
 };
 
+// EVD of G^T G from its tall factor Wt = G^T (n x l, overwritten by its QR
+// factor): the RandSVD / Nystrom tail (proj/src/sketch.cpp:27-33, :191-197).
+DeviceEVD evd_from_tall(DevBuf<double>& wt, long long n, int l, double shift, bool floor0, cudaStream_t st);
+
 // out = (I + V diag(lambda) V^T)^{-1} v (proj/src/linalg.cpp:32-50).
 void woodbury_apply(const DeviceEVD& e, const double* v, double* out, long long n, cudaStream_t st);
 
