@@ -11,7 +11,6 @@
 // Stencil/RK kernels are one thread per point; every formula keeps the
 // reference's operation order (proj/src/bve.cpp:28-82, :171-211), so the
 // tangent/adjoint match the reference's arithmetic to rounding.
-#include <cublas_v2.h>
 
 #include "bve3_kernels.cuh"
 #include "linalg_kernels.cuh"
@@ -136,10 +135,56 @@ __global__ void adj_stage_kernel(Bve3Args a, int stage, const double* __restrict
   else out[g] = lam[g] / 3.0 + 0.75 * t2[g] + L[g] + a.dt * o;
 }
 
-__global__ void scale_kernel(double* __restrict__ x, const double* __restrict__ s, long long dim, int nvec) {
-  const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (g >= dim * nvec) return;
-  x[g] *= s[g % dim];
+// Orthonormal sine transform along x of every row (proj/src/dirichlet.cpp:
+// 110-122 restricted to one dimension): out(i, j) = sum_k S(i, k) in(k, j),
+// S(i, k) = sqrt(2 / (nx + 1)) sin((i + 1)(k + 1) pi / (nx + 1)). One CTA per
+// row chunk; the row and the nx x nx table are staged in shared memory. S is
+// symmetric and orthogonal (S^2 = I), so the same kernel is its own inverse.
+__global__ void sine_x_kernel(int nx, int ny, const double* __restrict__ sx, const double* __restrict__ in,
+                              double* __restrict__ out, int rows_per_cta) {
+  extern __shared__ double sm3[];
+  double* tab = sm3;               // nx x nx
+  double* row = sm3 + nx * nx;     // rows_per_cta x nx
+  const long long dim = static_cast<long long>(nx) * ny;
+  const long long v = blockIdx.y;
+  const int j0 = blockIdx.x * rows_per_cta;
+  const int nr = min(rows_per_cta, ny - j0);
+  for (int e = threadIdx.x; e < nx * nx; e += blockDim.x) tab[e] = sx[e];
+  for (int e = threadIdx.x; e < nr * nx; e += blockDim.x)
+    row[e] = in[v * dim + static_cast<long long>(j0) * nx + e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < nr * nx; e += blockDim.x) {
+    const int r = e / nx, i = e % nx;
+    const double* rr = row + r * nx;
+    double acc = 0.0;
+    for (int k = 0; k < nx; ++k) acc = fma(tab[i + k * nx], rr[k], acc);
+    out[v * dim + static_cast<long long>(j0) * nx + e] = acc;
+  }
+}
+
+// Per x-mode i, the exact solve of the Dirichlet tridiagonal system in y,
+// ((a + bx mu_i) I + by tridiag(-1, 2, -1)) x = d (Thomas; the elimination
+// multipliers m[j][i] = 1 / pivot_j and c[j][i] = -by / pivot_j depend only on
+// the mode and are tabulated once). Same operator the reference diagonalises
+// by the sine transform in y (proj/src/dirichlet.cpp:82-99, :149-153).
+// Thread = mode, walking the ny rows (coalesced across the modes of a warp).
+__global__ void thomas_y_kernel(int nx, int ny, double off, const double* __restrict__ m, const double* __restrict__ c,
+                                double* __restrict__ x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nx) return;
+  double* f = x + static_cast<long long>(blockIdx.y) * nx * ny + i;
+  double prev = 0.0;
+  for (int j = 0; j < ny; ++j) {
+    const long long o = static_cast<long long>(j) * nx;
+    prev = (f[o] - off * prev) * m[o + i];
+    f[o] = prev;
+  }
+  double nxt = f[static_cast<long long>(ny - 1) * nx];
+  for (int j = ny - 2; j >= 0; --j) {
+    const long long o = static_cast<long long>(j) * nx;
+    nxt = f[o] - c[o + i] * nxt;
+    f[o] = nxt;
+  }
 }
 
 // alpha v + neg_laplacian_2d(v, b, b) (proj/src/prior.cpp:53-62)
@@ -157,65 +202,68 @@ __global__ void lap2_inv_sqrt_kernel(int nx, int ny, double alpha, double b, con
   out[g] = alpha * c + (b * (2.0 * c - f(i - 1, j) - f(i + 1, j)) + b * (2.0 * c - f(i, j - 1) - f(i, j + 1)));
 }
 
-void check_blas(cublasStatus_t s, const char* what) {
-  if (s != CUBLAS_STATUS_SUCCESS) throw CudaError(std::string("cuBLAS ") + what + " failed (" + std::to_string(s) + ")");
-}
-
 constexpr int kTpb = 256;
 int blocks(long long n) { return ceil_div(n, kTpb); }
 
 }  // namespace
 
 // ---------------------------------------------------------- DST solver --
-DstSolver::DstSolver(int nx, int ny, double a, double bx, double by, cudaStream_t st) : nx_(nx), ny_(ny), st_(st) {
-  // proj/src/dirichlet.cpp:82-120: orthonormal sine matrices and eigenvalues
+DstSolver::DstSolver(int nx, int ny, double a, double bx, double by, cudaStream_t st)
+    : nx_(nx), ny_(ny), off_(-by), st_(st) {
+  // proj/src/dirichlet.cpp:82-99: the operator must be positive definite
+  // (a + bx mu_x + by mu_y > 0 for every mode, mu = 2 - 2 cos(k pi / (n + 1))).
   auto mu = [](int k, int n) { return 2.0 - 2.0 * std::cos(static_cast<double>(k) * M_PI / (n + 1.0)); };
-  std::vector<double> inv(static_cast<size_t>(nx) * ny), sx(static_cast<size_t>(nx) * nx),
-      sy(static_cast<size_t>(ny) * ny);
   for (int j = 0; j < ny; ++j)
-    for (int i = 0; i < nx; ++i) {
-      const double lam = a + bx * mu(i + 1, nx) + by * mu(j + 1, ny);
-      if (!(lam > 0.0)) throw std::invalid_argument("DirichletSolver2D: operator is not positive definite");
-      inv[i + static_cast<size_t>(nx) * j] = 1.0 / lam;
+    for (int i = 0; i < nx; ++i)
+      if (!(a + bx * mu(i + 1, nx) + by * mu(j + 1, ny) > 0.0))
+        throw std::invalid_argument("DirichletSolver2D: operator is not positive definite");
+  // orthonormal sine matrix in x (proj/src/dirichlet.cpp:110-120)
+  std::vector<double> sx(static_cast<size_t>(nx) * nx);
+  const double nr = std::sqrt(2.0 / (nx + 1));
+  for (int i = 0; i < nx; ++i)
+    for (int k = 0; k < nx; ++k) sx[i + static_cast<size_t>(nx) * k] = nr * std::sin((i + 1.0) * (k + 1.0) * M_PI / (nx + 1));
+  // Thomas multipliers per x-mode for (a + bx mu_i + 2 by) on the diagonal, -by off it
+  std::vector<double> m(static_cast<size_t>(nx) * ny), c(static_cast<size_t>(nx) * ny);
+  for (int i = 0; i < nx; ++i) {
+    const double diag = a + bx * mu(i + 1, nx) + 2.0 * by;
+    double cp = 0.0;
+    for (int j = 0; j < ny; ++j) {
+      const double piv = diag - off_ * cp;
+      if (!(piv > 0.0)) throw std::invalid_argument("DirichletSolver2D: operator is not positive definite");
+      m[i + static_cast<size_t>(nx) * j] = 1.0 / piv;
+      cp = off_ / piv;
+      c[i + static_cast<size_t>(nx) * j] = cp;
     }
-  auto fill = [](std::vector<double>& s, int n) {
-    const double nr = std::sqrt(2.0 / (n + 1));
-    for (int i = 0; i < n; ++i)
-      for (int k = 0; k < n; ++k) s[i + static_cast<size_t>(n) * k] = nr * std::sin((i + 1.0) * (k + 1.0) * M_PI / (n + 1));
-  };
-  fill(sx, nx);
-  fill(sy, ny);
-  inv_.upload(inv.data(), inv.size(), st);
+  }
   sx_.upload(sx.data(), sx.size(), st);
-  sy_.upload(sy.data(), sy.size(), st);
-  check_blas(cublasCreate(&h_), "create");
-  check_blas(cublasSetStream(h_, st), "set stream");
+  m_.upload(m.data(), m.size(), st);
+  c_.upload(c.data(), c.size(), st);
 }
-DstSolver::~DstSolver() {
-  if (h_) cublasDestroy(h_);
-}
+DstSolver::~DstSolver() = default;
 
-// out = S_x [inv o (S_x in S_y)] S_y for nvec fields (in may alias out).
+size_t DstSolver::sine_smem(int rows) const { return sizeof(double) * (static_cast<size_t>(nx_) * nx_ + static_cast<size_t>(rows) * nx_); }
+
+// out = S_x T^{-1} S_x in, T^{-1} the per-mode tridiagonal solves in y
+// (= S_x [inv o (S_x in S_y)] S_y, the reference's dense-sine solve, up to
+// roundoff). Three launches, no library call; in may alias out.
 void DstSolver::solve(const double* in, double* out, int nvec) const {
   const long long dim = static_cast<long long>(nx_) * ny_;
   tmp_.ensure(static_cast<size_t>(dim) * nvec);
-  const double one = 1.0, zero = 0.0;
-  // T = S_x [F_1 .. F_s]: one nx x (ny s) product
-  check_blas(cublasDgemm(h_, CUBLAS_OP_N, CUBLAS_OP_N, nx_, ny_ * nvec, nx_, &one, sx_.get(), nx_, in, nx_, &zero,
-                         tmp_.get(), nx_),
-             "dgemm Sx");
-  // out_v = T_v S_y
-  check_blas(cublasDgemmStridedBatched(h_, CUBLAS_OP_N, CUBLAS_OP_N, nx_, ny_, ny_, &one, tmp_.get(), nx_, dim,
-                                       sy_.get(), ny_, 0, &zero, out, nx_, dim, nvec),
-             "dgemm Sy");
-  scale_kernel<<<blocks(dim * nvec), kTpb, 0, st_>>>(out, inv_.get(), dim, nvec);
+  constexpr int kRows = 8;
+  const size_t sm = sine_smem(kRows);
+  static const bool once = [] {
+    SDV_CUDA(cudaFuncSetAttribute(sine_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    return true;
+  }();
+  (void)once;
+  if (sm > 200 * 1024) throw std::invalid_argument("DirichletSolver2D: nx too large for the shared-memory sine table");
+  const dim3 gx(ceil_div(ny_, kRows), nvec);
+  sine_x_kernel<<<gx, kTpb, sm, st_>>>(nx_, ny_, sx_.get(), in, tmp_.get(), kRows);
   SDV_LAUNCH_CHECK();
-  check_blas(cublasDgemm(h_, CUBLAS_OP_N, CUBLAS_OP_N, nx_, ny_ * nvec, nx_, &one, sx_.get(), nx_, out, nx_, &zero,
-                         tmp_.get(), nx_),
-             "dgemm Sx");
-  check_blas(cublasDgemmStridedBatched(h_, CUBLAS_OP_N, CUBLAS_OP_N, nx_, ny_, ny_, &one, tmp_.get(), nx_, dim,
-                                       sy_.get(), ny_, 0, &zero, out, nx_, dim, nvec),
-             "dgemm Sy");
+  thomas_y_kernel<<<dim3(ceil_div(nx_, 64), nvec), 64, 0, st_>>>(nx_, ny_, off_, m_.get(), c_.get(), tmp_.get());
+  SDV_LAUNCH_CHECK();
+  sine_x_kernel<<<gx, kTpb, sm, st_>>>(nx_, ny_, sx_.get(), tmp_.get(), out, kRows);
+  SDV_LAUNCH_CHECK();
 }
 
 // ------------------------------------------------------------- launchers --

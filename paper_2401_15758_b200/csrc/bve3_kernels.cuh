@@ -1,8 +1,6 @@
 // Host-side interface of the reference-BVE kernels (bve3_kernels.cu).
 #pragma once
 
-#include <cublas_v2.h>
-
 #include "common.cuh"
 
 namespace sdv {
@@ -16,8 +14,10 @@ struct Bve3Args {
   const double* forcing = nullptr;  // [ny]: sin(pi y_j), y_j = -1 + (j+1) dy
 };
 
-// (a I + bx Lx + by Ly)^{-1} on the Dirichlet grid by the dense orthonormal
-// sine transforms (proj/src/dirichlet.cpp:82-155), batched fp64 GEMMs.
+// (a I + bx Lx + by Ly)^{-1} on the Dirichlet grid (proj/src/dirichlet.cpp:
+// 82-155): the orthonormal sine transform in x (shared-memory matvec kernel)
+// diagonalises Lx; per x-mode the system in y is tridiagonal and solved
+// exactly (Thomas, tabulated multipliers). Hand-written kernels, no library.
 class DstSolver {
  public:
   DstSolver(int nx, int ny, double a, double bx, double by, cudaStream_t st);
@@ -27,10 +27,11 @@ class DstSolver {
   void solve(const double* in, double* out, int nvec) const;  // in may alias out
 
  private:
+  size_t sine_smem(int rows) const;
   int nx_, ny_;
+  double off_;
   cudaStream_t st_;
-  cublasHandle_t h_ = nullptr;
-  DevBuf<double> inv_, sx_, sy_;
+  DevBuf<double> sx_, m_, c_;
   mutable DevBuf<double> tmp_;
 };
 

@@ -116,6 +116,43 @@ __global__ void __launch_bounds__(kRedThreads) coldot_partial_kernel(const doubl
   if (threadIdx.x == 0) part[static_cast<long long>(col) * nchunks + blockIdx.x] = s;
 }
 
+// ---- fused PCG updates (proj/src/linalg.cpp:52-106). Same grid, grid-stride
+// partition and fma order as dot_partial_kernel, so every dot equals dev_dot's
+// bit for bit; the axpy arithmetic equals axpby_kernel's.
+// q <- p + q; part <- partial sums of <p, q>
+__global__ void __launch_bounds__(kRedThreads) pcg_q_kernel(long long n, const double* __restrict__ p,
+                                                            double* __restrict__ q, double* __restrict__ part) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (long long i = blockIdx.x * static_cast<long long>(kRedThreads) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * kRedThreads) {
+    const double pi = p[i];
+    const double qi = fma(1.0, pi, 1.0 * q[i]);
+    q[i] = qi;
+    s = fma(pi, qi, s);
+  }
+  s = block_sum<kRedThreads>(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+// alpha = rz / *pq; x <- x + alpha p; r <- r - alpha q; part <- partial sums of <r, r>
+__global__ void __launch_bounds__(kRedThreads) pcg_xr_kernel(long long n, double rz, const double* __restrict__ pq,
+                                                             const double* __restrict__ p, const double* __restrict__ q,
+                                                             double* __restrict__ x, double* __restrict__ r,
+                                                             double* __restrict__ part) {
+  __shared__ double sh[32];
+  const double alpha = rz / *pq;
+  double s = 0.0;
+  for (long long i = blockIdx.x * static_cast<long long>(kRedThreads) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * kRedThreads) {
+    x[i] = fma(alpha, p[i], 1.0 * x[i]);
+    const double ri = fma(-alpha, q[i], 1.0 * r[i]);
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  s = block_sum<kRedThreads>(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
 __global__ void axpby_kernel(long long n, double alpha, const double* __restrict__ x, double beta,
                              double* __restrict__ y) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
@@ -330,6 +367,21 @@ void dev_coldots(const double* a, long long lda, const double* b, long long ldb,
   SDV_LAUNCH_CHECK();
 }
 
+void dev_pcg_q(long long n, const double* p, double* q, double* pq, cudaStream_t st) {
+  DevBuf<double>& part = partial_buf(kRedBlocks, st);
+  pcg_q_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, p, q, part.get());
+  sum_partials_kernel<<<1, kRedThreads, 0, st>>>(part.get(), kRedBlocks, 1, pq);
+  count_launch(2);
+  SDV_LAUNCH_CHECK();
+}
+void dev_pcg_xr(long long n, double rz, const double* pq, const double* p, const double* q, double* x, double* r,
+                double* rr, cudaStream_t st) {
+  DevBuf<double>& part = partial_buf(kRedBlocks, st);
+  pcg_xr_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(n, rz, pq, p, q, x, r, part.get());
+  sum_partials_kernel<<<1, kRedThreads, 0, st>>>(part.get(), kRedBlocks, 1, rr);
+  count_launch(2);
+  SDV_LAUNCH_CHECK();
+}
 void dev_axpby(long long n, double alpha, const double* x, double beta, double* y, cudaStream_t st) {
   axpby_kernel<<<grid_for(n), 256, 0, st>>>(n, alpha, x, beta, y);
   count_launch();

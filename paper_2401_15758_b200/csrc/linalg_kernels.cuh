@@ -48,6 +48,11 @@ void dev_dot(const double* a, const double* b, long long n, double* out, cudaStr
 // Column dots: out[j] = sum_i a[i + j*lda] * b[i + j*ldb], j < ncols.
 void dev_coldots(const double* a, long long lda, const double* b, long long ldb, long long n, int ncols, double* out,
                  cudaStream_t st);
+// Fused PCG steps (dots bitwise equal to dev_dot): q <- p + q and *pq = <p, q>;
+// alpha = rz / *pq (device), x <- x + alpha p, r <- r - alpha q, *rr = <r, r>.
+void dev_pcg_q(long long n, const double* p, double* q, double* pq, cudaStream_t st);
+void dev_pcg_xr(long long n, double rz, const double* pq, const double* p, const double* q, double* x, double* r,
+                double* rr, cudaStream_t st);
 // y = alpha x + beta y   (alpha/beta host scalars)
 void dev_axpby(long long n, double alpha, const double* x, double beta, double* y, cudaStream_t st);
 // y = alpha x + beta y with alpha = (*num / *den) * sa (device scalars), used by PCG without host sync.

@@ -613,6 +613,9 @@ SketchResult adaptive_lanczos(MisfitOp& h, const SketchCfg& cfg, const double* s
 // ------------------------------------------------------------------ PCG -----
 // proj/src/linalg.cpp:52-106 on (I + H).
 PCGResult pcg_solve(MisfitOp& h, const double* b, const DeviceEVD* pre, double tol, int max_iter, double* x) {
+  // proj/src/linalg.cpp:52-106. One host read per iteration: the fused
+  // kernels leave <p, q>, <r, r> and <r, z> in a device scalar block and the
+  // host applies the reference's checks in the reference's order.
   if (!(tol > 0.0)) throw std::invalid_argument("pcg_solve: tolerance must be positive");
   const long long n = h.n();
   cudaStream_t st = h.stream();
@@ -624,33 +627,37 @@ PCGResult pcg_solve(MisfitOp& h, const double* b, const DeviceEVD* pre, double t
     return res;
   }
   DevBuf<double> r(static_cast<size_t>(n)), z(static_cast<size_t>(n)), p(static_cast<size_t>(n)),
-      q(static_cast<size_t>(n));
+      q(static_cast<size_t>(n)), sc(3);
   copy_dev(r.get(), b, n, st);
+  // unpreconditioned: z = r (no copy; <r, z> = <r, r>)
+  const double* zp = pre ? z.get() : r.get();
   if (pre) woodbury_apply(*pre, r.get(), z.get(), n, st);
-  else copy_dev(z.get(), r.get(), n, st);
-  double rz = host_dot(r.get(), z.get(), n, st);
+  double rz = host_dot(r.get(), zp, n, st);
   if (rz <= 0.0) throw std::runtime_error("pcg_solve: preconditioner is not positive definite (<r, M^-1 r> <= 0)");
-  copy_dev(p.get(), z.get(), n, st);
+  copy_dev(p.get(), zp, n, st);
+  double hs[3];
   for (int k = 1; k <= max_iter; ++k) {
     h.gram(p.get(), 1, q.get());
-    dev_axpby(n, 1.0, p.get(), 1.0, q.get(), st);
-    const double pq = host_dot(p.get(), q.get(), n, st);
+    dev_pcg_q(n, p.get(), q.get(), sc.get(), st);                                   // q = p + Hp, <p, q>
+    dev_pcg_xr(n, rz, sc.get(), p.get(), q.get(), x, r.get(), sc.get() + 1, st);  // x, r updates, <r, r>
+    if (pre) {
+      woodbury_apply(*pre, r.get(), z.get(), n, st);
+      dev_dot(r.get(), z.get(), n, sc.get() + 2, st);
+    }
+    SDV_CUDA(cudaMemcpyAsync(hs, sc.get(), sizeof(double) * (pre ? 3 : 2), cudaMemcpyDeviceToHost, st));
+    SDV_CUDA(cudaStreamSynchronize(st));
+    const double pq = hs[0];
     if (pq <= 0.0) throw std::runtime_error("pcg_solve: operator is not positive definite (<p, A p> <= 0)");
-    const double alpha = rz / pq;
-    dev_axpby(n, alpha, p.get(), 1.0, x, st);
-    dev_axpby(n, -alpha, q.get(), 1.0, r.get(), st);
-    const double relres = host_norm(r.get(), n, st) / rhs_norm;
+    const double relres = std::sqrt(hs[1]) / rhs_norm;
     res.relres.push_back(relres);
     res.iterations = k;
     if (relres <= tol) {
       res.converged = true;
       return res;
     }
-    if (pre) woodbury_apply(*pre, r.get(), z.get(), n, st);
-    else copy_dev(z.get(), r.get(), n, st);
-    const double rzn = host_dot(r.get(), z.get(), n, st);
+    const double rzn = pre ? hs[2] : hs[1];
     if (rzn <= 0.0) throw std::runtime_error("pcg_solve: preconditioner is not positive definite (<r, M^-1 r> <= 0)");
-    dev_axpby(n, 1.0, z.get(), rzn / rz, p.get(), st);
+    dev_axpby(n, 1.0, zp, rzn / rz, p.get(), st);
     rz = rzn;
   }
   return res;

@@ -9,6 +9,11 @@ oracle solves (minutes to tens of minutes of serial PCG on the host) would not
 fit the test budget. Short cases stay live in the other parity tests.
 
 Usage: ORACLE_THREADS=8 python tests/golden/make_golden.py [case ...]
+       ORACLE_BUILD=alt ORACLE_THREADS=8 python tests/golden/make_golden.py [case ...]
+The second form runs the oracle's second build (oracle/Makefile ALTFLAGS,
+FMA contraction) and writes gn_<name>_alt.npz: the roundoff spread of the
+reference algorithm between two valid builds, which bounds the PCG-count and
+analysis agreement the GPU can be held to on long CG runs.
 (ORACLE_THREADS only speeds the oracle up: its threading is bitwise neutral,
 tests/test_oracle.py::test_oracle_threading_bitwise_neutral.)
 """
@@ -42,10 +47,13 @@ CASES = {
 }
 
 
+ALT = os.environ.get("ORACLE_BUILD") == "alt"
+
+
 def oracle_flags():
     mk = os.path.join(os.path.dirname(os.path.dirname(HERE)), "oracle", "Makefile")
     for line in open(mk):
-        if line.startswith("CXXFLAGS"):
+        if line.startswith("ALTFLAGS" if ALT else "CXXFLAGS"):
             return line.split("=", 1)[1].strip()
     return "?"
 
@@ -62,7 +70,7 @@ def run(name):
                 host=platform.processor() or platform.machine(),
                 git=subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True, text=True,
                                    cwd=HERE).stdout.strip())
-    out = os.path.join(HERE, f"gn_{name}.npz")
+    out = os.path.join(HERE, f"gn_{name}{'_alt' if ALT else ''}.npz")
     np.savez_compressed(out, analysis=r["analysis"], log=r["log"], summary=r["summary"], eig0=r["eig0"],
                         meta=json.dumps(meta))
     print(f"{name}: {len(r['log'])} GN iterations, PCG {r['log'][:, 4].astype(int).tolist()}, "

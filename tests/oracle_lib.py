@@ -13,7 +13,10 @@ import subprocess
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LIB_PATH = os.path.join(ROOT, "oracle", "_build", "libsdv_oracle.so")
+# ORACLE_BUILD=alt selects the second build (oracle/Makefile ALTFLAGS: -O3
+# -march=native -ffp-contract=fast): same algorithm, different rounding.
+LIB_PATH = os.path.join(ROOT, "oracle", "_build",
+                        "libsdv_oracle_alt.so" if os.environ.get("ORACLE_BUILD") == "alt" else "libsdv_oracle.so")
 
 _lib = None
 

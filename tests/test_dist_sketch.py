@@ -117,14 +117,14 @@ def test_sharded_randsvd_two_ranks_gloo_equals_single_process(cfg, steps, l):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cfg,steps,l,world", [(0, -1, 30, 2), (2, 20, 12, 3), (3, 8, 110, 2)])
-def test_sharded_randsvd_threads_on_gpu(oracle, sdv, cfg, steps, l, world):
+@pytest.mark.parametrize("cfg,steps,spi,l,world", [(0, -1, -1, 30, 2), (2, 20, -1, 12, 3), (3, 8, 4, 110, 2)])
+def test_sharded_randsvd_threads_on_gpu(oracle, sdv, cfg, steps, spi, l, world):
     """Sharded RandSVD eigenvalues equal the single-process device sketch and
     the oracle's to <= 1e-10 (the shards run narrower blocks, so other kernel
     paths: agreement is to roundoff, not bitwise)."""
     from test_gpu_parity import eig_rel, pair
 
-    osc, prob = pair(oracle, cfg, steps)
+    osc, prob = pair(oracle, cfg, steps, spi)
     gtr = prob.linearize(osc.background)
     seed = oracle.mix_seed(2, 0x736b6574636800)
     eg, bg, _ = gtr.sketch(0, l, seed)
