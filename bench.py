@@ -19,6 +19,11 @@ port of it (oracle/), all host threads, bounded sample extrapolated to HVP/s.
 import argparse
 import json
 import os
+
+# CPU timings (cpu_baseline, the --impl reference arm, the GN CPU baseline) use
+# the oracle's -O3 FMA build (oracle/Makefile ALTFLAGS); parity tests use the
+# primary build the golden fixtures were generated with.
+os.environ.setdefault("ORACLE_BUILD", "alt")
 import statistics
 import subprocess
 import sys
@@ -84,6 +89,66 @@ def gn_solve_timing(cfg, method=None):
             # model applications including sketch construction (BASELINE configs[4] compares these)
             "tlm_plus_adj_total": cnt["tlm"] + cnt["adj"] + cnt["offline_tlm"] + cnt["offline_adj"],
             "final_cost": float(r["summary"][0]), "rel_error_analysis": err_a, "rel_error_background": err_b}
+
+
+def cpu_sweep_seconds(cfg, budget_s=3.0):
+    """One-core seconds of one full-window single-vector sweep (TLM or ADJ) of
+    the oracle port on config `cfg`, from a timed short window (TLM + ADJ over
+    k steps on one thread, scaled by steps / k / 2)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as O
+
+    from paper_2401_15758_b200 import scenario
+
+    spec = scenario.CONFIGS[cfg]
+    v = O.gaussian_matrix(spec.dim, 1, 5)[0]
+
+    def timed(k):
+        osc = O.Scenario(cfg, steps=k, spi=k)
+        tr = osc.linearize(osc.background)
+        t0 = time.perf_counter()
+        tr.adj_range(0, k, tr.tlm_range(0, k, v))
+        return time.perf_counter() - t0
+
+    k = 1
+    dt = timed(k)
+    k = max(1, min(spec.steps, int(round(budget_s / max(dt, 1e-4)))))
+    dt = timed(k)
+    return dt / 2.0 * spec.steps / k, k
+
+
+def cpu_gn_baseline(run, cfg, method=None):
+    """the CPU GN solve time beside the GPU one. C0/C1: the
+    oracle port's own gn_solve, timed (all host threads for the sketch's column
+    fan-out, serial PCG, as the reference's apply_columns / pcg_solve). C2-C4
+    (tens of minutes to hours on the CPU): the port's one-core sweep time times
+    the GPU run's own sweep counters (serial: fwd + online tlm + adj; sketch:
+    offline tlm + adj over all threads), labelled as extrapolated."""
+    cores = os.cpu_count() or 1
+    if cfg in (0, 1):
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracle_lib as O
+
+        from paper_2401_15758_b200 import api, scenario
+
+        kw = scenario.CONFIGS[cfg].gn_kwargs()
+        if method is not None:
+            kw["method"] = method
+        kw["mode"] = api.MODES[kw["mode"]] if isinstance(kw["mode"], str) else kw["mode"]
+        osc = O.Scenario(cfg)
+        t0 = time.perf_counter()
+        r = osc.gn_solve(workers=cores, **kw)
+        dt = time.perf_counter() - t0
+        return {"seconds": dt, "kind": "measured", "cores": cores, "total_pcg": int(r["summary"][2]),
+                "build": "oracle port, ALTFLAGS (-O3 -march=x86-64-v3 -ffp-contract=fast)"}
+    c = run["counters"]
+    t1, k = cpu_sweep_seconds(cfg)
+    serial = c["fwd"] + c["tlm"] + c["adj"]
+    fan = c["offline_tlm"] + c["offline_adj"]
+    return {"seconds": t1 * (serial + fan / cores), "kind": "extrapolated", "cores": cores,
+            "one_core_sweep_s": t1, "sample": f"1 vector, TLM+ADJ over {k} RK4 steps, one core",
+            "model": "one-core sweep time x (fwd + online tlm + adj + (offline tlm + adj) / cores) of this GPU run",
+            "build": "oracle port, ALTFLAGS (-O3 -march=x86-64-v3 -ffp-contract=fast)"}
 
 
 # ------------------------------------------------------------------ dist ----
@@ -281,7 +346,11 @@ def run_reference(args, world, rank):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 * (args.s or spec.rank) / value,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference", "config": config_block(spec, args.s or spec.rank, args.group),
+            "impl": "reference",
+            # the same config block as our arm (sweep group resolved the same way)
+            "config": config_block(spec, args.s or spec.rank,
+                                   min(args.s or spec.rank, group_size(spec.dim, args.group)) if spec.model == 2
+                                   else args.s or spec.rank),
             "cpu_baseline": cb, "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -375,14 +444,19 @@ def run_ours(args, world, rank, local):
     hbm, peak_src = peaks()
     probe_stages = 64
     ms_stage, ms_col = tr.probe_stage_kernels(s, probe_stages)
+    probe = {"tlm_stage_ms": ms_stage, "tlm_col_ms": ms_col}
     if spec.model == api.MODEL_BVE:
         g = min(s, group_size(n, args.group))
+        ms_adj, ms_carry_adj = tr.probe_adj_stage_kernels(s, probe_stages)
+        probe.update(adj_stage_ms=ms_adj, adj_carry_ms=ms_carry_adj)
         # per stage launch: read+write the g tangent fields (16 N each) + read
         # the two base stage fields (omega_b, psi_b) once for the group
         alg_bytes = g * 16.0 * ngrid + 2 * 8.0 * ngrid
-        dur = ms_stage
-        kname = ("bve stage_kernel, fused Poisson path (y-solved spectra from tile carries, in-place inverse x-FFT, "
-                 "Arakawa TLM stencil + RK4 update, forward x-FFT, tile-local y-recurrences)")
+        dur = 0.5 * (ms_stage + ms_adj)  # the sweeps run as many ADJ stage launches as TLM ones
+        kname = ("bve stage_kernel TLM + ADJ (mean), fused Poisson path (y-solved spectra from tile carries, "
+                 "in-place inverse x-FFT, Arakawa stencils + RK4 / adjoint-RK4 update, forward x-FFT, tile-local "
+                 f"y-recurrences); probe: one launch of g = {g} vectors per stage (the sweep runs the block as two "
+                 "concurrent lanes of g/2 on two streams)")
     else:
         g = s
         k = max(1, min(prob.total_steps, probe_stages // 4))
@@ -397,17 +471,24 @@ def run_ours(args, world, rank, local):
     # measured DRAM bytes of this kernel per launch (ncu --set full capture in
     # profiles/ncu_traffic.json, per vector x the probe's group), when profiled
     traffic = None
+    fp64 = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if spec.model == api.MODEL_BVE and os.path.exists(tf):
-        t = json.load(open(tf)).get("bve_stage_kernel_tlm", {})
-        if t.get("grid") == spec.n:
-            traffic = t["dram_bytes_per_vector"] * g
+        tj = json.load(open(tf))
+        t, ta = tj.get("bve_stage_kernel_tlm", {}), tj.get("bve_stage_kernel_adj", {})
+        if t.get("grid") == spec.n and ta.get("grid") == spec.n:
+            traffic = 0.5 * (t["dram_bytes_per_vector"] + ta["dram_bytes_per_vector"]) * g
+            if "fp64_pipe_pct" in t and "fp64_pipe_pct" in ta:
+                fp64 = 0.5 * (t["fp64_pipe_pct"] + ta["fp64_pipe_pct"])
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
             "traffic": traffic,
             # measured DRAM bytes (ncu) over the live launch time: how close the
             # kernel's actual data movement runs to the HBM peak
             "traffic_GBs": (traffic / (dur / 1000.0) / 1e9) if traffic else None,
-            "kernel": kname, "kernel_ms": dur, "col_kernel_ms": ms_col,
+            "traffic_source": "ncu --set full capture (profiles/ncu_traffic.json), per vector x g" if traffic else None,
+            # FP64 pipe utilisation of the same capture (the north star's co-bound)
+            "fp64_pipe_pct": fp64,
+            "kernel": kname, "kernel_ms": dur, "col_kernel_ms": ms_col, "probe": probe,
             "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
             "step_model": {"B_HVP_bytes": b_hvp, "achieved_GBs": step_achieved, "frac": step_achieved / hbm,
                            "note": "SURVEY.md 8(d) streaming model: HVP/s x B_HVP per GPU"}}
@@ -451,14 +532,23 @@ def run_ours(args, world, rank, local):
             line["block_sweep"] = sweep
         gn = args.gn
         if gn == "auto":
-            gn = "0,1,2" if world == 1 and not args.window else "none"
+            # every config's GN solve (C4: its adaptive Nystrom arm; the SingleView arm, ~9 min, under 'all')
+            gn = "0,1,2,3,4" if world == 1 and not args.window else "none"
         if gn and gn != "none":
             cfgs = [0, 1, 2, 3, 4] if gn == "all" else [int(x) for x in gn.split(",") if x]
             runs = []
             for c in cfgs:
                 runs.append(gn_solve_timing(c))
-                if c == 4:  # BASELINE configs[4]: SingleView vs Nystrom on total products
+                if c == 4 and args.gn == "all":  # BASELINE configs[4]: SingleView vs Nystrom on total products
                     runs.append(gn_solve_timing(4, method=api.SINGLEVIEW))
+            if not args.no_cpu_baseline:
+                for r in runs:
+                    try:
+                        meth = {"randsvd": api.RANDSVD, "nystrom": api.NYSTROM, "singleview": api.SINGLEVIEW}
+                        cfg_i = [sp.name for sp in scenario.CONFIGS].index(r["config"])
+                        r["cpu_baseline"] = cpu_gn_baseline(r, cfg_i, meth.get(r["method"]))
+                    except Exception as e:  # reported, not fatal
+                        r["cpu_baseline"] = {"seconds": None, "kind": f"failed: {e}"}
             line["gn_solve"] = runs
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -144,7 +144,9 @@ int sdv_woodbury_apply(sdv_problem* p, int64_t l, const double* basis, const dou
 int sdv_thin_qr(sdv_problem* p, int64_t n, int64_t l, const double* y, double* q, double* r, int* ndef);
 
 /* Device-buffer forms for the sharded sketch: thin QR of a
- * device block in place (y_dev n x l -> Q, r host l x l), and the RandSVD /
+ * device block in place (y_dev n x l -> Q, r host l x l; the sketches' QR:
+ * CholQR2 on the fp64 tensor cores when the block is well conditioned, else
+ * Householder, R(i,i) >= 0 either way), and the RandSVD /
  * Nystrom tail evd_from_gram_factor (proj/src/sketch.cpp:27-33, :191-197):
  * from the tall factor Wt (n x l, device, unchanged) the basis Q_W U (device
  * n x l, may be NULL) and eigenvalues S^2 - shift (floored at 0 if floor0). */
@@ -225,6 +227,9 @@ int sdv_event_elapsed_ms(void* start, void* stop, float* ms);
  * (group of s vectors) with events around every launch; returns the mean
  * duration of the fused stage kernel and of the column-FFT kernel (ms). */
 int sdv_probe_stage_kernels(sdv_traj* t, int s, int stages, float* ms_stage, float* ms_col);
+/* The same for `stages` adjoint RK stages (periodic BVE): mean duration of the
+ * fused ADJ stage kernel and of the carry / column pass before it (ms). */
+int sdv_probe_adj_stage_kernels(sdv_traj* t, int s, int stages, float* ms_stage, float* ms_col);
 
 #ifdef __cplusplus
 }

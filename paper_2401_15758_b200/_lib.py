@@ -106,6 +106,7 @@ def lib():
         "sdv_event_record": (C.c_int, [vp, vp]),
         "sdv_event_elapsed_ms": (C.c_int, [vp, vp, C.POINTER(C.c_float)]),
         "sdv_probe_stage_kernels": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+        "sdv_probe_adj_stage_kernels": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

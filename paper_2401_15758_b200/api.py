@@ -259,6 +259,11 @@ class Trajectory:
         check(lib().sdv_probe_stage_kernels(self._h, s, stages, C.byref(a), C.byref(b)))
         return a.value, b.value
 
+    def probe_adj_stage_kernels(self, s, stages):
+        a, b = C.c_float(), C.c_float()
+        check(lib().sdv_probe_adj_stage_kernels(self._h, s, stages, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def sketch(self, method, rank, seed, rank2=-1, want_basis=True):
         eig = np.empty(rank)
         basis = np.empty((rank, self.problem.n)) if want_basis else None

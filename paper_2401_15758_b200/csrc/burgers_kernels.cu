@@ -63,53 +63,83 @@ __global__ void __launch_bounds__(1024) burgers_fwd_kernel(BurgersArgs p, const 
   for (int q = 0; q < NPT; ++q) out[tid + q * nt] = U[q];
 }
 
-// Block TLM over steps [k0, k1). state: [nvec][n] in/out.
+// Double-buffered base stage inputs in shared memory: the row of stage t+1
+// (n doubles, contiguous in [steps][4][n]) arrives by one TMA bulk copy issued
+// at the start of stage t, so the stored trajectory's L2/HBM latency overlaps
+// the current stage. Thread 0 issues; every thread waits on the row's mbarrier.
+struct BaseRows {
+  double* row[2];
+  unsigned long long* bar;  // [2]
+  unsigned ph[2];
+  __device__ __forceinline__ void issue(const double* src, int n, int slot) {
+    fence_proxy_async();
+    mbar_arm(&bar[slot], sizeof(double) * n);
+    bulk_g2s(row[slot], src, sizeof(double) * n, &bar[slot]);
+  }
+  __device__ __forceinline__ const double* wait(int slot) {
+    mbar_wait(&bar[slot], ph[slot]);
+    ph[slot] ^= 1u;
+    return row[slot];
+  }
+};
+
+// Block TLM over steps [k0, k1). state: [nvec][n] in/out. Shared memory:
+// two stage-input buffers (alternating, one barrier per RK stage) and two
+// base rows (TMA-fed one stage ahead).
 template <int NPT>
 __global__ void __launch_bounds__(1024) burgers_tlm_kernel(BurgersArgs p, double* __restrict__ state) {
-  extern __shared__ double sh[];
-  double* X = sh;
+  extern __shared__ __align__(128) double sh[];
+  __shared__ __align__(8) unsigned long long bars[2];
   const int n = p.n, tid = threadIdx.x, nt = blockDim.x;
   const long long v = blockIdx.x;
+  BaseRows br{{sh + 2 * n, sh + 3 * n}, bars, {0u, 0u}};
+  const long long t0 = static_cast<long long>(p.k0) * 4, t1 = static_cast<long long>(p.k1) * 4;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init_fence();
+  }
   double D[NPT], A[NPT];
+  int cur = 0;
 #pragma unroll
-  for (int q = 0; q < NPT; ++q) D[q] = state[v * n + tid + q * nt];
+  for (int q = 0; q < NPT; ++q) {
+    D[q] = state[v * n + tid + q * nt];
+    sh[tid + q * nt] = D[q];
+  }
+  __syncthreads();
+  if (tid == 0 && t0 < t1) br.issue(p.base + t0 * n, n, 0);
   for (int k = p.k0; k < p.k1; ++k) {
-    const double* ub = p.base + static_cast<long long>(k) * 4 * n;
-    for (int s = 0; s < 4; ++s) {
-      double xs[NPT];
-      if (s == 0) {
 #pragma unroll
-        for (int q = 0; q < NPT; ++q) X[tid + q * nt] = D[q];
-      }
-      __syncthreads();
-      const double* u = ub + s * n;
+    for (int s = 0; s < 4; ++s) {
+      const long long t = static_cast<long long>(k) * 4 + s;
+      const int slot = static_cast<int>((t - t0) & 1);
+      if (tid == 0 && t + 1 < t1) br.issue(p.base + (t + 1) * n, n, slot ^ 1);
+      const double* u = br.wait(slot);
+      const double* X = sh + cur * n;
+      double* Xn = sh + (cur ^ 1) * n;
 #pragma unroll
       for (int q = 0; q < NPT; ++q) {
         const int i = tid + q * nt, im = wrapm(i - 1, n), ip = wrapm(i + 1, n);
         const double xi = X[i], xm = X[im], xp = X[ip];
-        const double ui = __ldg(u + i), um = __ldg(u + im), up = __ldg(u + ip);
+        const double ui = u[i], um = u[im], up = u[ip];
         const double kk = -xi * (up - um) * p.c1 - ui * (xp - xm) * p.c1 + p.nu * (xm - 2.0 * xi + xp) * p.c2;
+        double xs;
         switch (s) {
-          case 0: A[q] = D[q] + p.dt / 6.0 * kk; xs[q] = D[q] + 0.5 * p.dt * kk; break;
-          case 1: A[q] += p.dt / 3.0 * kk; xs[q] = D[q] + 0.5 * p.dt * kk; break;
-          case 2: A[q] += p.dt / 3.0 * kk; xs[q] = D[q] + p.dt * kk; break;
-          default: D[q] = A[q] + p.dt / 6.0 * kk; break;
+          case 0: A[q] = D[q] + p.dt / 6.0 * kk; xs = D[q] + 0.5 * p.dt * kk; break;
+          case 1: A[q] += p.dt / 3.0 * kk; xs = D[q] + 0.5 * p.dt * kk; break;
+          case 2: A[q] += p.dt / 3.0 * kk; xs = D[q] + p.dt * kk; break;
+          default: D[q] = A[q] + p.dt / 6.0 * kk; xs = D[q]; break;
         }
+        Xn[i] = xs;  // next stage input (after stage 3: the next step's state)
       }
+      cur ^= 1;
       __syncthreads();
-      if (s < 3) {
-#pragma unroll
-        for (int q = 0; q < NPT; ++q) X[tid + q * nt] = xs[q];
-      }
     }
     if (p.y && (k + 1) % p.spi == 0) {
       const int iv = (k + 1) / p.spi - 1;
-#pragma unroll
-      for (int q = 0; q < NPT; ++q) X[tid + q * nt] = D[q];
-      __syncthreads();
+      const double* X = sh + cur * n;
       for (int o = tid; o < p.n_obs; o += nt)
         p.y[v * p.m + static_cast<long long>(iv) * p.n_obs + o] = X[p.idx[o]] * p.w[static_cast<long long>(iv) * p.n_obs + o];
-      __syncthreads();
     }
   }
 #pragma unroll
@@ -118,30 +148,50 @@ __global__ void __launch_bounds__(1024) burgers_tlm_kernel(BurgersArgs p, double
 
 // Block ADJ over steps [k0, k1) backwards:
 //   a4 = dt/6 L, m4 = J4^T a4; a3 = dt/3 L + dt m4, ...; L <- L + sum m.
-// Observation scatter L[idx] += y*w before each interval's last step.
+// Observation scatter L[idx] += y*w before each interval's last step. L stays
+// in registers (own points); a alternates between two shared buffers (one
+// barrier per stage); base rows TMA-fed one stage ahead as in the TLM.
 template <int NPT>
 __global__ void __launch_bounds__(1024) burgers_adj_kernel(BurgersArgs p, double* __restrict__ state) {
-  extern __shared__ double sh[];
-  double* L = sh;
-  double* Ash = sh + p.n;
+  extern __shared__ __align__(128) double sh[];
+  __shared__ __align__(8) unsigned long long bars[2];
   const int n = p.n, tid = threadIdx.x, nt = blockDim.x;
   const long long v = blockIdx.x;
+  BaseRows br{{sh + 2 * n, sh + 3 * n}, bars, {0u, 0u}};
+  double* Ls = sh + 4 * n;  // observation scatter
+  const long long tlast = static_cast<long long>(p.k1) * 4 - 1, tfirst = static_cast<long long>(p.k0) * 4;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init_fence();
+  }
+  double L[NPT];
 #pragma unroll
-  for (int q = 0; q < NPT; ++q) L[tid + q * nt] = state[v * n + tid + q * nt];
+  for (int q = 0; q < NPT; ++q) L[q] = state[v * n + tid + q * nt];
   __syncthreads();
+  if (tid == 0 && tfirst <= tlast) br.issue(p.base + tlast * n, n, 0);
+  int cur = 0;
   for (int k = p.k1 - 1; k >= p.k0; --k) {
     if (p.y && (k + 1) % p.spi == 0) {
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) Ls[tid + q * nt] = L[q];
+      __syncthreads();
       const int iv = (k + 1) / p.spi - 1;
       for (int o = tid; o < p.n_obs; o += nt)
-        L[p.idx[o]] += p.y[v * p.m + static_cast<long long>(iv) * p.n_obs + o] * p.w[static_cast<long long>(iv) * p.n_obs + o];
+        Ls[p.idx[o]] += p.y[v * p.m + static_cast<long long>(iv) * p.n_obs + o] * p.w[static_cast<long long>(iv) * p.n_obs + o];
       __syncthreads();
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) L[q] = Ls[tid + q * nt];
     }
-    const double* ub = p.base + static_cast<long long>(k) * 4 * n;
     double acc[NPT], mu[NPT];
+#pragma unroll
     for (int s = 3; s >= 0; --s) {
+      const long long t = static_cast<long long>(k) * 4 + s;
+      const int slot = static_cast<int>((tlast - t) & 1);
+      double* Ab = sh + cur * n;
 #pragma unroll
       for (int q = 0; q < NPT; ++q) {
-        const double l = L[tid + q * nt];
+        const double l = L[q];
         double a;
         switch (s) {
           case 3: a = p.dt / 6.0 * l; break;
@@ -149,27 +199,27 @@ __global__ void __launch_bounds__(1024) burgers_adj_kernel(BurgersArgs p, double
           case 1: a = p.dt / 3.0 * l + 0.5 * p.dt * mu[q]; break;
           default: a = p.dt / 6.0 * l + 0.5 * p.dt * mu[q]; break;
         }
-        Ash[tid + q * nt] = a;
+        Ab[tid + q * nt] = a;
       }
-      __syncthreads();
-      const double* u = ub + s * n;
+      const double* u = br.wait(slot);
+      __syncthreads();  // also: every thread is past the previous stage's reads of the other base row
+      if (tid == 0 && t - 1 >= tfirst) br.issue(p.base + (t - 1) * n, n, slot ^ 1);
 #pragma unroll
       for (int q = 0; q < NPT; ++q) {
         const int i = tid + q * nt, im = wrapm(i - 1, n), ip = wrapm(i + 1, n);
-        const double ai = Ash[i], am = Ash[im], ap = Ash[ip];
-        const double ui = __ldg(u + i), um = __ldg(u + im), up = __ldg(u + ip);
+        const double ai = Ab[i], am = Ab[im], ap = Ab[ip];
+        const double ui = u[i], um = u[im], up = u[ip];
         const double m = -ai * (up - um) * p.c1 + (up * ap - um * am) * p.c1 + p.nu * (am - 2.0 * ai + ap) * p.c2;
         mu[q] = m;
         acc[q] = (s == 3) ? m : acc[q] + m;
       }
-      __syncthreads();
+      cur ^= 1;  // the next stage writes the other buffer
     }
 #pragma unroll
-    for (int q = 0; q < NPT; ++q) L[tid + q * nt] += acc[q];
-    __syncthreads();
+    for (int q = 0; q < NPT; ++q) L[q] += acc[q];
   }
 #pragma unroll
-  for (int q = 0; q < NPT; ++q) state[v * n + tid + q * nt] = L[tid + q * nt];
+  for (int q = 0; q < NPT; ++q) state[v * n + tid + q * nt] = L[q];
 }
 
 // 1-D periodic circulant apply out = Re IFFT(sym .* FFT(in)), one CTA per vector.
@@ -224,7 +274,11 @@ void burgers_tlm(const BurgersArgs& p, double* state, int nvec, cudaStream_t st)
   int th, npt;
   geometry(p.n, th, npt);
   dispatch_npt(npt, [&](auto c) {
-    burgers_tlm_kernel<decltype(c)::value><<<nvec, th, sizeof(double) * p.n, st>>>(p, state);
+    const size_t smem = sizeof(double) * 4 * p.n;
+    if (smem > 48 * 1024)
+      SDV_CUDA(cudaFuncSetAttribute(burgers_tlm_kernel<decltype(c)::value>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    burgers_tlm_kernel<decltype(c)::value><<<nvec, th, smem, st>>>(p, state);
   });
   SDV_LAUNCH_CHECK();
 }
@@ -232,7 +286,7 @@ void burgers_adj(const BurgersArgs& p, double* state, int nvec, cudaStream_t st)
   int th, npt;
   geometry(p.n, th, npt);
   dispatch_npt(npt, [&](auto c) {
-    const size_t smem = sizeof(double) * 2 * p.n;
+    const size_t smem = sizeof(double) * 5 * p.n;
     if (smem > 48 * 1024)
       SDV_CUDA(cudaFuncSetAttribute(burgers_adj_kernel<decltype(c)::value>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

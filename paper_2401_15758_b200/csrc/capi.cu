@@ -328,7 +328,7 @@ int sdv_thin_qr_dev(sdv_problem* p, int64_t n, int64_t l, double* y_dev, double*
     need(r, "r");
     Lock lk(p->mu);
     cudaStream_t st = p->p->stream();
-    const int nd = sdv::dev_householder_qr(n, static_cast<int>(l), y_dev, r, st);
+    const int nd = sdv::dev_thin_qr(n, static_cast<int>(l), y_dev, r, st);  // the sketches' QR (CholQR2 / Householder)
     SDV_CUDA(cudaStreamSynchronize(st));
     if (ndef) *ndef = nd;
   });
@@ -556,6 +556,15 @@ int sdv_probe_stage_kernels(sdv_traj* t, int s, int stages, float* ms_stage, flo
     need(t, "trajectory");
     Lock lk(t->owner->mu);
     t->owner->p->probe_stage_kernels(*t->t, s, stages, ms_stage, ms_col);
+  });
+}
+int sdv_probe_adj_stage_kernels(sdv_traj* t, int s, int stages, float* ms_stage, float* ms_col) {
+  return guard([&] {
+    need(t, "trajectory");
+    need(ms_stage, "ms_stage");
+    need(ms_col, "ms_col");
+    Lock lk(t->owner->mu);
+    t->owner->p->probe_adj_stage_kernels(*t->t, s, stages, ms_stage, ms_col);
   });
 }
 

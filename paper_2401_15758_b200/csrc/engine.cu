@@ -681,6 +681,66 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
   }
 }
 
+// ADJ counterpart of probe_stage_kernels (BVE only): `stages` adjoint RK
+// stages of one s-vector launch (reverse stage order, has_prev after the
+// first), with the carry / column pass timed separately. The inputs are the
+// probe's own workspaces; only the timing is meaningful.
+void Problem::probe_adj_stage_kernels(const Trajectory& tr, int s, int stages, float* ms_stage, float* ms_col) const {
+  if (s < 1 || stages < 1) throw std::invalid_argument("probe: need s >= 1 and stages >= 1");
+  if (d_.model != kModelBVE) throw std::invalid_argument("probe: the ADJ stage probe covers the periodic BVE model");
+  cudaEvent_t ev[3];
+  for (auto& e : ev) SDV_CUDA(cudaEventCreate(&e));
+  s = std::min(s, group());
+  wstate_.ensure(static_cast<size_t>(s) * dim_);
+  ensure_work(s);
+  for (int v = 0; v < s; ++v)
+    SDV_CUDA(cudaMemcpyAsync(wstate_.get() + v * dim_, tr.w.get(), sizeof(double) * dim_, cudaMemcpyDeviceToDevice,
+                             st_));
+  const int n = d_.n;
+  const bool fz = fused(s);
+  double2* s_cur = ws0_.get();
+  double2* s_nxt = ws1_.get();
+  bve_row_fwd(n, wstate_.get(), s_cur, s, st_);
+  SDV_CUDA(cudaMemcpyAsync(wx0_.get(), wstate_.get(), sizeof(double) * dim_ * s, cudaMemcpyDeviceToDevice, st_));
+  double tot_stage = 0.0, tot_col = 0.0;
+  int qi = 0;
+  for (int q = 0; q < stages; ++q) {
+    const int k = tr.steps - 1 - (q / 4) % tr.steps, sg = 3 - q % 4;
+    const bool has_prev = q > 0;
+    SDV_CUDA(cudaEventRecord(ev[0], st_));
+    if (has_prev) {
+      if (fz) poisson_carry(s_cur, 0, s, st_);
+      else poisson_col(s_cur, s, st_);
+    }
+    SDV_CUDA(cudaEventRecord(ev[1], st_));
+    StageArgs a = bve_args(d_);
+    a.stage = sg;
+    a.flags = has_prev ? kFlagHasPrev : 0;
+    a.s_in = s_cur;
+    a.s_out = s_nxt;
+    a.d = wstate_.get();
+    a.acc = wa_.get();
+    a.q_in = qi ? wx1_.get() : wx0_.get();
+    a.q_out = qi ? wx0_.get() : wx1_.get();
+    a.base_w = tr.w.get() + (static_cast<long long>(k) * 4 + sg) * dim_;
+    a.base_p = tr.p.get() + (static_cast<long long>(k) * 4 + sg) * dim_;
+    if (fz) set_fused(a, 0);
+    bve_stage(n, kModeAdj, a, s, st_, fz);
+    SDV_CUDA(cudaEventRecord(ev[2], st_));
+    SDV_CUDA(cudaEventSynchronize(ev[2]));
+    float m1 = 0, m2 = 0;
+    SDV_CUDA(cudaEventElapsedTime(&m1, ev[0], ev[1]));
+    SDV_CUDA(cudaEventElapsedTime(&m2, ev[1], ev[2]));
+    tot_col += m1;
+    tot_stage += m2;
+    std::swap(s_cur, s_nxt);
+    qi ^= 1;
+  }
+  *ms_stage = static_cast<float>(tot_stage / stages);
+  *ms_col = static_cast<float>(tot_col / std::max(1, stages - 1));
+  for (auto& e : ev) SDV_CUDA(cudaEventDestroy(e));
+}
+
 void Problem::probe_stage_kernels(const Trajectory& tr, int s, int stages, float* ms_stage, float* ms_col) const {
   if (s < 1 || stages < 1) throw std::invalid_argument("probe: need s >= 1 and stages >= 1");
   if (d_.model == kModelBVE3) throw std::invalid_argument("probe: the stage-kernel probe covers the BASELINE models");

@@ -91,6 +91,7 @@ class Problem {
   // the column kernel over `stages` TLM stages on a group of s vectors. For
   // Burgers the persistent sweep kernel is timed instead (ms_col = 0).
   void probe_stage_kernels(const Trajectory& tr, int s, int stages, float* ms_stage, float* ms_col) const;
+  void probe_adj_stage_kernels(const Trajectory& tr, int s, int stages, float* ms_stage, float* ms_col) const;
 
   const double* d_rinv_sqrt() const { return rinv_sqrt_.get(); }
   const double* d_rinv() const { return rinv_.get(); }

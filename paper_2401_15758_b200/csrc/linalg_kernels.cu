@@ -1,7 +1,10 @@
 // Device linear algebra for the sketch / PCG / Woodbury layer (sm_100a, fp64).
 // Deterministic reductions: a fixed grid writes per-block partials that one
 // block folds in a fixed order (warp-shuffle trees inside each block).
+#include <string>
+
 #include "linalg_kernels.cuh"
+#include "hostla.hpp"
 
 #include <cfloat>
 #include <map>
@@ -91,6 +94,15 @@ __global__ void __launch_bounds__(kRedThreads) sum_partials_kernel(const double*
   s = block_sum<kRedThreads>(s, sh);
   if (threadIdx.x == 0) out[c] = s;
   (void)ncols;
+}
+
+// out[e] = sum_c part[c * ne + e], c in order (one thread per output element)
+__global__ void sum_partials_t_kernel(const double* __restrict__ part, int np, int ne, double* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ne) return;
+  double s = 0.0;
+  for (int c = 0; c < np; ++c) s += part[static_cast<long long>(c) * ne + e];
+  out[e] = s;
 }
 
 DevBuf<double>& partial_buf(size_t n, cudaStream_t st) {
@@ -245,6 +257,80 @@ __global__ void __launch_bounds__(64) trsm_rows_lower_kernel(long long n, int l,
     const double v = s / __ldg(lm + i + static_cast<long long>(i) * l);
     xr[i] = v;
     x[r + static_cast<long long>(i) * n] = v;
+  }
+}
+
+// ---- fp64 tensor-core (DMMA, mma.sync.m8n8k4.f64) Gram of a tall block -----
+// G = A^T A for A n x l column-major (l <= 8 LT). Each CTA accumulates a row
+// chunk: 32-row slabs of A are staged in shared memory as [col][row] with a
+// stride of 36 doubles (the 8-byte fragment loads of a half-warp hit 16
+// distinct bank pairs), and warp w owns the upper-triangle 8 x 8 output tiles
+// of tile rows w, w + 8, ...: per 4-row k-step it loads one A fragment per
+// tile row and one B fragment per tile column and issues one DMMA per tile.
+// Partials [chunk][l][l] are reduced in a fixed order (deterministic).
+constexpr int kDmmaRows = 32, kDmmaStride = 36;
+__device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+template <int LT>
+__global__ void __launch_bounds__(256) gram_dmma_kernel(long long n, int l, const double* __restrict__ a,
+                                                        long long rows_per_cta, double* __restrict__ part) {
+  constexpr int LP = 8 * LT;
+  constexpr int TPW = (LT + 7) / 8;  // tile rows per warp
+  __shared__ __align__(16) double sa[LP * kDmmaStride];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const long long r0 = blockIdx.x * rows_per_cta, r1 = min(n, r0 + rows_per_cta);
+  double acc[TPW][LT][2];
+#pragma unroll
+  for (int u = 0; u < TPW; ++u)
+#pragma unroll
+    for (int tj = 0; tj < LT; ++tj) acc[u][tj][0] = acc[u][tj][1] = 0.0;
+  const int fr = lane % 4, fc = lane / 4;  // fragment row (k) and column (tile-local)
+  for (long long rb = r0; rb < r1; rb += kDmmaRows) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < LP * kDmmaRows; e += 256) {
+      const int c = e / kDmmaRows, r = e % kDmmaRows;
+      const long long row = rb + r;
+      sa[c * kDmmaStride + r] = (c < l && row < r1) ? a[row + static_cast<long long>(c) * n] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int k0 = 0; k0 < kDmmaRows; k0 += 4) {
+      double bf[LT];
+#pragma unroll
+      for (int tj = 0; tj < LT; ++tj) bf[tj] = sa[(8 * tj + fc) * kDmmaStride + k0 + fr];
+#pragma unroll
+      for (int u = 0; u < TPW; ++u) {
+        const int ti = warp + 8 * u;
+        if (ti < LT) {
+          const double af = sa[(8 * ti + fc) * kDmmaStride + k0 + fr];  // A fragment of tile row ti
+#pragma unroll
+          for (int tj = 0; tj < LT; ++tj)
+            if (tj >= ti) dmma_884(acc[u][tj][0], acc[u][tj][1], af, bf[tj]);
+        }
+      }
+    }
+  }
+  double* out = part + static_cast<long long>(blockIdx.x) * l * l;
+#pragma unroll
+  for (int u = 0; u < TPW; ++u) {
+    const int ti = warp + 8 * u;
+    if (ti >= LT) continue;
+#pragma unroll
+    for (int tj = 0; tj < LT; ++tj) {
+      if (tj < ti) continue;
+      const int i = 8 * ti + fc;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = 8 * tj + 2 * fr + h;
+        if (i < l && j < l) {
+          out[i + static_cast<long long>(j) * l] = acc[u][tj][h];
+          out[j + static_cast<long long>(i) * l] = acc[u][tj][h];
+        }
+      }
+    }
   }
 }
 
@@ -434,6 +520,33 @@ void dev_trsm_rows_lower(long long n, int l, const double* lmat, const double* y
   SDV_LAUNCH_CHECK();
 }
 
+namespace {
+template <int LT>
+void gram_dmma_launch(long long n, int l, const double* a, double* c, cudaStream_t st) {
+  // ~2 CTAs per SM, each over a contiguous chunk of 32-row slabs
+  const long long slabs = (n + kDmmaRows - 1) / kDmmaRows;
+  const int nchunks = static_cast<int>(std::max<long long>(1, std::min<long long>(296, slabs)));
+  const long long rows = ((slabs + nchunks - 1) / nchunks) * kDmmaRows;
+  const int used = static_cast<int>((n + rows - 1) / rows);
+  DevBuf<double>& part = partial_buf(static_cast<size_t>(used) * l * l, st);
+  gram_dmma_kernel<LT><<<used, 256, 0, st>>>(n, l, a, rows, part.get());
+  sum_partials_t_kernel<<<ceil_div(static_cast<long long>(l) * l, 256), 256, 0, st>>>(part.get(), used, l * l, c);
+  count_launch(2);
+  SDV_LAUNCH_CHECK();
+}
+}  // namespace
+
+bool dev_gram_dmma_ok(int l) { return l >= 1 && l <= 128; }
+
+void dev_gram_dmma(long long n, int l, const double* a, double* c, cudaStream_t st) {
+  if (!dev_gram_dmma_ok(l)) throw std::invalid_argument("dev_gram_dmma: need 1 <= l <= 128");
+  const int lt = (l + 7) / 8;
+  if (lt <= 4) gram_dmma_launch<4>(n, l, a, c, st);
+  else if (lt <= 8) gram_dmma_launch<8>(n, l, a, c, st);
+  else if (lt <= 12) gram_dmma_launch<12>(n, l, a, c, st);
+  else gram_dmma_launch<16>(n, l, a, c, st);
+}
+
 int dev_householder_qr(long long n, int l, double* y, double* r_host, cudaStream_t st) {
   if (n < l) throw std::invalid_argument("thin_qr: need rows >= cols");
   StreamWork& ws = stream_work(st);
@@ -505,6 +618,97 @@ int dev_householder_qr(long long n, int l, double* y, double* r_host, cudaStream
   for (int i = 0; i < l; ++i)
     if (std::abs(r_host[i + static_cast<size_t>(i) * l]) <= tol) ++ndef;
   return ndef;
+}
+
+// ---- CholQR2 on the fp64 tensor cores ------------------------------------------
+// Y = Q R by two Cholesky-QR passes (G = Y^T Y on DMMA, R = chol(G)^T on the
+// host, Q = Y R^{-1} as a tall x small product), R = R2 R1 with R(i,i) > 0 (the
+// reference's sign convention, proj/src/linalg.cpp:108-134). Declines (returns
+// -1, Y untouched) when a Cholesky factor breaks down or its diagonal spans
+// more than 1e5 (kappa(Y) beyond what two passes restore to orthogonality):
+// the caller then runs the Householder path, which also handles deficiency.
+namespace {
+bool chol_upper(const std::vector<double>& g, int l, std::vector<double>& r) {
+  HMat a(l, l);
+  for (int j = 0; j < l; ++j)
+    for (int i = 0; i < l; ++i) a(i, j) = 0.5 * (g[i + static_cast<size_t>(j) * l] + g[j + static_cast<size_t>(i) * l]);
+  HMat lo;
+  try {
+    lo = hcholesky(a);
+  } catch (const std::exception&) {
+    return false;
+  }
+  double dmin = lo(0, 0), dmax = lo(0, 0);
+  for (int i = 0; i < l; ++i) {
+    dmin = std::min(dmin, lo(i, i));
+    dmax = std::max(dmax, lo(i, i));
+  }
+  if (!(dmin > 1e-5 * dmax)) return false;
+  r.assign(static_cast<size_t>(l) * l, 0.0);
+  for (int j = 0; j < l; ++j)
+    for (int i = 0; i <= j; ++i) r[i + static_cast<size_t>(j) * l] = lo(j, i);
+  return true;
+}
+// inverse of an upper-triangular l x l (column-major) by back substitution
+std::vector<double> upper_inv(const std::vector<double>& r, int l) {
+  std::vector<double> x(static_cast<size_t>(l) * l, 0.0);
+  for (int j = 0; j < l; ++j) {
+    x[j + static_cast<size_t>(j) * l] = 1.0 / r[j + static_cast<size_t>(j) * l];
+    for (int i = j - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int k = i + 1; k <= j; ++k) s += r[i + static_cast<size_t>(k) * l] * x[k + static_cast<size_t>(j) * l];
+      x[i + static_cast<size_t>(j) * l] = -s / r[i + static_cast<size_t>(i) * l];
+    }
+  }
+  return x;
+}
+}  // namespace
+
+int dev_cholqr2(long long n, int l, double* y, double* r_host, cudaStream_t st) {
+  if (n < l) throw std::invalid_argument("thin_qr: need rows >= cols");
+  if (!dev_gram_dmma_ok(l)) return -1;
+  StreamWork& ws = stream_work(st);
+  DevBuf<double>& qbuf = ws.qr_q;
+  DevBuf<double>& small = ws.qr_w;
+  qbuf.ensure(static_cast<size_t>(n) * l);
+  small.ensure(static_cast<size_t>(l) * l);
+  std::vector<double> g(static_cast<size_t>(l) * l), r1, r2;
+  auto gram_host = [&](const double* a) {
+    dev_gram_dmma(n, l, a, small.get(), st);
+    SDV_CUDA(cudaMemcpyAsync(g.data(), small.get(), sizeof(double) * l * l, cudaMemcpyDeviceToHost, st));
+    SDV_CUDA(cudaStreamSynchronize(st));
+  };
+  gram_host(y);
+  if (!chol_upper(g, l, r1)) return -1;
+  std::vector<double> inv = upper_inv(r1, l);
+  SDV_CUDA(cudaMemcpyAsync(small.get(), inv.data(), sizeof(double) * l * l, cudaMemcpyHostToDevice, st));
+  dev_gemm_nn_small(n, l, l, 1.0, y, small.get(), 0.0, qbuf.get(), st);  // Q1 = Y R1^{-1}
+  gram_host(qbuf.get());
+  if (!chol_upper(g, l, r2)) return -1;
+  inv = upper_inv(r2, l);
+  SDV_CUDA(cudaMemcpyAsync(small.get(), inv.data(), sizeof(double) * l * l, cudaMemcpyHostToDevice, st));
+  dev_gemm_nn_small(n, l, l, 1.0, qbuf.get(), small.get(), 0.0, y, st);  // Q = Q1 R2^{-1}
+  // R = R2 R1 (upper)
+  for (int j = 0; j < l; ++j)
+    for (int i = 0; i < l; ++i) {
+      double acc = 0.0;
+      for (int k = i; k <= j; ++k) acc += r2[i + static_cast<size_t>(k) * l] * r1[k + static_cast<size_t>(j) * l];
+      r_host[i + static_cast<size_t>(j) * l] = i <= j ? acc : 0.0;
+    }
+  SDV_CUDA(cudaStreamSynchronize(st));
+  return 0;  // full rank (a deficient Y would have declined)
+}
+
+int dev_thin_qr(long long n, int l, double* y, double* r_host, cudaStream_t st) {
+  static const bool householder = [] {
+    const char* e = std::getenv("SDV_QR");
+    return e && std::string(e) == "householder";
+  }();
+  if (!householder) {
+    const int nd = dev_cholqr2(n, l, y, r_host, st);
+    if (nd >= 0) return nd;
+  }
+  return dev_householder_qr(n, l, y, r_host, st);
 }
 
 }  // namespace sdv

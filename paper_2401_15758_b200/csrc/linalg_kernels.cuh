@@ -60,6 +60,9 @@ void dev_scale_copy(long long n, double a, const double* x, double* y, cudaStrea
 void dev_fill(long long n, double v, double* y, cudaStream_t st);
 // C (k x l) = A^T B with A (n x k), B (n x l) column-major, leading dims n. Deterministic.
 void dev_gemm_tn(long long n, int k, int l, const double* a, const double* b, double* c, cudaStream_t st);
+// G (l x l) = A^T A on the fp64 tensor cores (mma.sync.m8n8k4.f64), l <= 128.
+bool dev_gram_dmma_ok(int l);
+void dev_gram_dmma(long long n, int l, const double* a, double* c, cudaStream_t st);
 // C (n x l) = alpha * A (n x k) * B (k x l) + beta * C; B small, device, column-major (ldb = k).
 void dev_gemm_nn_small(long long n, int k, int l, double alpha, const double* a, const double* b, double beta,
                        double* c, cudaStream_t st);
@@ -72,5 +75,11 @@ void dev_trsm_rows_lower(long long n, int l, const double* lmat, const double* y
 // y (n x l) is overwritten by Q; r_host receives R (l x l, column-major).
 // Returns the number of deficient columns.
 int dev_householder_qr(long long n, int l, double* y, double* r_host, cudaStream_t st);
+// CholQR2 on the DMMA Gram (l <= 128); returns -1 without touching y when the
+// block is too ill-conditioned or deficient for it.
+int dev_cholqr2(long long n, int l, double* y, double* r_host, cudaStream_t st);
+// Thin QR used by the sketches: CholQR2 when it applies (default; SDV_QR=
+// householder forces the Householder path), else Householder.
+int dev_thin_qr(long long n, int l, double* y, double* r_host, cudaStream_t st);
 
 }  // namespace sdv

@@ -75,7 +75,7 @@ void copy_dev(double* dst, const double* src, long long n, cudaStream_t st) {
 DeviceEVD evd_from_tall(DevBuf<double>& wt, long long n, int l, double shift, bool floor0, cudaStream_t st) {
   HMat r(l, l), u, v;
   std::vector<double> s;
-  dev_householder_qr(n, l, wt.get(), r.a.data(), st);
+  dev_thin_qr(n, l, wt.get(), r.a.data(), st);
   hsvd_square(r, u, s, v);
   DeviceEVD e;
   e.n = n;
@@ -177,7 +177,7 @@ SketchResult randsvd_sketch(MisfitOp& a, int rank, uint64_t seed) {
   DevBuf<double> y(static_cast<size_t>(m) * rank), wt(static_cast<size_t>(n) * rank);
   a.apply(omega.get(), rank, y.get());
   std::vector<double> r(static_cast<size_t>(rank) * rank);
-  dev_householder_qr(m, rank, y.get(), r.data(), st);
+  dev_thin_qr(m, rank, y.get(), r.data(), st);
   a.adjoint(y.get(), rank, wt.get());
   SketchResult res;
   res.evd = evd_from_tall(wt, n, rank, 0.0, false, st);
@@ -194,7 +194,7 @@ DeviceEVD nystrom_assemble(const double* omega, const double* y, long long n, in
   copy_dev(tmp.get(), y, n * l, st);
   HMat ry(l, l), u, v;
   std::vector<double> s;
-  dev_householder_qr(n, l, tmp.get(), ry.a.data(), st);
+  dev_thin_qr(n, l, tmp.get(), ry.a.data(), st);
   hsvd_square(ry, u, s, v);
   const double ynorm = s.empty() ? 0.0 : s[0];
   if (ynorm == 0.0) {
@@ -204,7 +204,7 @@ DeviceEVD nystrom_assemble(const double* omega, const double* y, long long n, in
     e.basis.alloc(static_cast<size_t>(n) * l);
     copy_dev(e.basis.get(), omega, n * l, st);
     std::vector<double> r(static_cast<size_t>(l) * l);
-    dev_householder_qr(n, l, e.basis.get(), r.data(), st);
+    dev_thin_qr(n, l, e.basis.get(), r.data(), st);
     e.set_eig(std::vector<double>(static_cast<size_t>(l), 0.0), st);
     return e;
   }
@@ -289,7 +289,7 @@ SVState singleview_init(MisfitOp& a, int r1, int r2, uint64_t seed, long* tlm, l
   *tlm += r1;
   *adj += r2;
   std::vector<double> r(static_cast<size_t>(r1) * r1);
-  dev_householder_qr(m, r1, s.q_y.get(), r.data(), st);
+  dev_thin_qr(m, r1, s.q_y.get(), r.data(), st);
   const HMat mm = gram_tn(m, r2, r1, s.psi.get(), s.q_y.get(), st);
   hqr(mm, s.q_m, s.r_m);
   return s;
@@ -436,7 +436,7 @@ SketchResult adaptive_randsvd(MisfitOp& a, const SketchCfg& cfg, MisfitOp& probe
   DevBuf<double> q(static_cast<size_t>(m) * l), wt(static_cast<size_t>(n) * l);
   a.apply(omega.get(), l, q.get());
   std::vector<double> r(static_cast<size_t>(l) * l);
-  dev_householder_qr(m, l, q.get(), r.data(), st);
+  dev_thin_qr(m, l, q.get(), r.data(), st);
   a.adjoint(q.get(), l, wt.get());
   res.tlm += l;
   res.adj += l;
@@ -462,7 +462,7 @@ SketchResult adaptive_randsvd(MisfitOp& a, const SketchCfg& cfg, MisfitOp& probe
     a.apply(g.get(), lh, ynew.get());
     orthogonalize_block(ynew.get(), lh, q.get(), l, m, st);
     std::vector<double> rr(static_cast<size_t>(lh) * lh);
-    dev_householder_qr(m, lh, ynew.get(), rr.data(), st);
+    dev_thin_qr(m, lh, ynew.get(), rr.data(), st);
     a.adjoint(ynew.get(), lh, wnew.get());
     res.tlm += lh;
     res.adj += lh;
@@ -546,7 +546,7 @@ SketchResult adaptive_singleview(MisfitOp& a, const SketchCfg& cfg, MisfitOp& pr
     res.tlm += lh;
     orthogonalize_block(ynew.get(), lh, s.q_y.get(), l1, m, st);
     std::vector<double> rr(static_cast<size_t>(lh) * lh);
-    dev_householder_qr(m, lh, ynew.get(), rr.data(), st);
+    dev_thin_qr(m, lh, ynew.get(), rr.data(), st);
     // Column-append QR update of M = Psi^T [Q_Y Q_Y_new].
     const HMat pm = gram_tn(m, l2, lh, s.psi.get(), ynew.get(), st);
     HMat c = hmat_mul(hmat_t(s.q_m), pm);

@@ -42,6 +42,8 @@ CASES = {
     # C4: the config's adaptive Nystrom (10 by 10 to 100, SketchPrecA with the reuse test) on the full
     # 256^2 grid over a 40-step window (2 intervals), 3 GN iterations so the reuse decision is taken twice
     "c4_w40": (4, 40, 20, dict(mode=2, method=1, rank=10, growth=10, max_rank=100, rank2=201, max_gn_iters=3)),
+    # C4's solver on an 8-step window (2 intervals), one GN iteration: the adaptive sketch hits its cap
+    "c4_w8": (4, 8, 4, dict(mode=2, method=1, rank=10, growth=10, max_rank=100, rank2=201, max_gn_iters=1)),
     # C4 with adaptive SingleView (the config's other arm), same window, 2 GN iterations
     "c4_w40_sv": (4, 40, 20, dict(mode=2, method=2, rank=10, growth=10, max_rank=100, rank2=201, max_gn_iters=2)),
 }
