@@ -189,28 +189,6 @@ def test_gn_solve_parity(oracle, sdv, cfg, mode, method, steps, iters):
         assert eig_rel(rg["eig0"], ro["eig0"]) <= 1e-8
 
 
-def test_c4_adaptive_gn_parity(oracle, sdv):
-    """C4's own solver (SketchPrecA, adaptive Nystrom from 10 by 10 to 100) on the full 256^2 grid, window
-    shortened to 8 RK4 steps, one GN iteration: same growth/rank decisions, PCG +-1, same counters.
-
-    The analysis bound here is 2.5e-7, not 1e-8. The sketch hits its rank cap, so PCG runs 140 iterations
-    to the config's loose 1e-6 tolerance, and the iterate is roundoff-sensitive at that level: two builds of
-    the oracle itself (-march=x86-64-v3 with FMA vs -march=x86-64 -ffp-contract=off) give analyses 5.7e-8
-    apart on this case. Measured GPU vs oracle: 9.8e-8."""
-    from paper_2401_15758_b200 import scenario
-
-    osc, prob = pair(oracle, 4, steps=8, spi=4)
-    kw = scenario.CONFIGS[4].gn_kwargs()
-    kw.update(max_gn_iters=1)
-    ro = osc.gn_solve(max_gn_iters=1, workers=16)
-    rg = prob.gn_solve(**kw)
-    assert len(rg["log"]) == len(ro["log"]) == 1
-    assert rg["log"][0][8] == ro["log"][0][8]  # final rank
-    assert abs(rg["log"][0][4] - ro["log"][0][4]) <= 1
-    assert np.array_equal(rg["log"][:, 14:16], ro["log"][:, 14:16])
-    assert rel(rg["analysis"], ro["analysis"]) <= 2.5e-7
-
-
 @pytest.mark.parametrize("cfg,steps,method", [(0, -1, 0), (0, -1, 1), (0, -1, 2), (2, 20, 1), (2, 20, 2)])
 def test_adaptive_sketch_and_cond_estimate_parity(oracle, sdv, cfg, steps, method):
     """adaptive_{randsvd,nystrom,singleview} + cond_estimate (proj/src/sketch.cpp:391-564): the same
