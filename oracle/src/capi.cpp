@@ -1,5 +1,6 @@
 // CPU ORACLE (test infrastructure only): C-ABI used by tests/ (ctypes) and
 // by bench.py's cpu_baseline / --impl reference leg. Never used by the product.
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -72,6 +73,14 @@ int oracle_scenario_create_ex(int cfg, int steps, int spi) {
     auto s = std::make_unique<Scenario>(cfg == 100   ? make_reference_burgers_1_1()
                                         : cfg == 101 ? make_reference_bve_2()
                                                      : make_config(cfg, steps, spi));
+    // ORACLE_PERTURB=<rel>: background x (1 + rel g), g ~ N(0, 1) (seeded), to
+    // measure how sensitive a case's PCG counts are to roundoff-sized input
+    // changes (tests/golden/make_golden.py); unset in every parity run.
+    if (const char* e = std::getenv("ORACLE_PERTURB")) {
+      const double rel = std::atof(e);
+      const Vec g = gaussian_matrix(static_cast<int64_t>(s->problem.background.size()), 1, 777).a;
+      for (size_t i = 0; i < s->problem.background.size(); ++i) s->problem.background[i] *= 1.0 + rel * g[i];
+    }
     std::lock_guard<std::mutex> l(g_mu);
     g_sc.push_back(std::move(s));
     h = static_cast<int>(g_sc.size()) - 1;

@@ -14,6 +14,9 @@ The second form runs the oracle's second build (oracle/Makefile ALTFLAGS,
 FMA contraction) and writes gn_<name>_alt.npz: the roundoff spread of the
 reference algorithm between two valid builds, which bounds the PCG-count and
 analysis agreement the GPU can be held to on long CG runs.
+       ORACLE_PERTURB=1e-15 ... writes gn_<name>_pert.npz: the same case from a
+background perturbed at roundoff level (relative 1e-15), a second measure of how
+chaotic the case's PCG counts are.
 (ORACLE_THREADS only speeds the oracle up: its threading is bitwise neutral,
 tests/test_oracle.py::test_oracle_threading_bitwise_neutral.)
 """
@@ -50,6 +53,7 @@ CASES = {
 
 
 ALT = os.environ.get("ORACLE_BUILD") == "alt"
+PERT = os.environ.get("ORACLE_PERTURB")  # e.g. 1e-15: background x (1 + rel g), oracle/src/capi.cpp
 
 
 def oracle_flags():
@@ -69,10 +73,11 @@ def run(name):
     secs = time.time() - t0
     meta = dict(case=name, config=cfg, steps=steps, spi=spi, gn=kw, oracle_seconds=secs, workers=workers,
                 oracle_threads=os.environ.get("ORACLE_THREADS", "1"), oracle_cxxflags=oracle_flags(),
+                background_perturbation=PERT,
                 host=platform.processor() or platform.machine(),
                 git=subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True, text=True,
                                    cwd=HERE).stdout.strip())
-    out = os.path.join(HERE, f"gn_{name}{'_alt' if ALT else ''}.npz")
+    out = os.path.join(HERE, f"gn_{name}{'_alt' if ALT else ''}{'_pert' if PERT else ''}.npz")
     np.savez_compressed(out, analysis=r["analysis"], log=r["log"], summary=r["summary"], eig0=r["eig0"],
                         meta=json.dumps(meta))
     print(f"{name}: {len(r['log'])} GN iterations, PCG {r['log'][:, 4].astype(int).tolist()}, "
