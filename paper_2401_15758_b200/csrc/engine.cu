@@ -545,23 +545,39 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
 }
 
 std::vector<Problem::Lane> Problem::split_lanes(int v0, int gn) const {
-  // Two concurrent lanes (streams) per group when it holds >= 2 vectors.
+  // Concurrent lanes (streams) per group: two by default when it holds >= 2
+  // vectors (SDV_LANES=k for k lanes, SDV_ONE_LANE for one), near-equal widths.
   std::vector<Lane> lanes;
-  const bool two = gn >= 2 && !std::getenv("SDV_ONE_LANE");
-  if (!two) {
+  static const int nl_env = [] {
+    if (std::getenv("SDV_ONE_LANE")) return 1;
+    const char* e = std::getenv("SDV_LANES");
+    return e ? std::max(1, std::min(8, std::atoi(e))) : 2;
+  }();
+  const int nl = std::min(nl_env, gn);
+  if (nl <= 1) {
     lanes.push_back(Lane{v0, gn, 0, st_});
     lanes.back().fz = fused(gn);
     lanes.back().lite = !lanes.back().fz && d_.model == kModelBVE && bve_lite_ok(d_.n, gn);
     return lanes;
   }
-  if (!st2_) SDV_CUDA(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking));
+  while (static_cast<int>(lane_st_.size()) < nl - 1) {
+    cudaStream_t s2;
+    cudaEvent_t e2;
+    SDV_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    SDV_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+    lane_st_.push_back(s2);
+    lane_ev_.push_back(e2);
+  }
   if (!ev_fork_) SDV_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
-  if (!ev_join_) SDV_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   SDV_CUDA(cudaEventRecord(ev_fork_, st_));
-  SDV_CUDA(cudaStreamWaitEvent(st2_, ev_fork_, 0));
-  const int a = (gn + 1) / 2;
-  lanes.push_back(Lane{v0, a, 0, st_});
-  lanes.push_back(Lane{v0 + a, gn - a, a, st2_});
+  int off = 0;
+  for (int i = 0; i < nl; ++i) {
+    const int cnt = gn / nl + (i < gn % nl ? 1 : 0);
+    cudaStream_t st = i == 0 ? st_ : lane_st_[i - 1];
+    if (i > 0) SDV_CUDA(cudaStreamWaitEvent(st, ev_fork_, 0));
+    lanes.push_back(Lane{v0 + off, cnt, off, st});
+    off += cnt;
+  }
   for (auto& L : lanes) {
     L.fz = fused(L.cnt);
     L.lite = !L.fz && d_.model == kModelBVE && bve_lite_ok(d_.n, L.cnt);
@@ -570,9 +586,10 @@ std::vector<Problem::Lane> Problem::split_lanes(int v0, int gn) const {
 }
 
 void Problem::join_lanes(const std::vector<Lane>& lanes) const {
-  if (lanes.size() < 2) return;
-  SDV_CUDA(cudaEventRecord(ev_join_, st2_));
-  SDV_CUDA(cudaStreamWaitEvent(st_, ev_join_, 0));
+  for (size_t i = 1; i < lanes.size(); ++i) {
+    SDV_CUDA(cudaEventRecord(lane_ev_[i - 1], lanes[i].st));
+    SDV_CUDA(cudaStreamWaitEvent(st_, lane_ev_[i - 1], 0));
+  }
 }
 
 void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1, const double* y,
@@ -893,10 +910,10 @@ void Problem::clear_graphs() const {
 Problem::~Problem() {
   clear_graphs();
   if (ev_fork_) cudaEventDestroy(ev_fork_);
-  if (ev_join_) cudaEventDestroy(ev_join_);
-  if (st2_) {
-    release_stream_work(st2_);
-    cudaStreamDestroy(st2_);
+  for (auto e : lane_ev_) cudaEventDestroy(e);
+  for (auto s2 : lane_st_) {
+    release_stream_work(s2);
+    cudaStreamDestroy(s2);
   }
   if (st_) {
     release_stream_work(st_);

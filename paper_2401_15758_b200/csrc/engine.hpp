@@ -155,8 +155,9 @@ class Problem {
   };
   std::vector<Lane> split_lanes(int v0, int gn) const;
   void join_lanes(const std::vector<Lane>& lanes) const;
-  mutable cudaStream_t st2_ = nullptr;
-  mutable cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  mutable std::vector<cudaStream_t> lane_st_;  // lanes 1.. of a sweep group (lane 0 runs on st_)
+  mutable std::vector<cudaEvent_t> lane_ev_;
+  mutable cudaEvent_t ev_fork_ = nullptr;
 
  public:
   ~Problem();

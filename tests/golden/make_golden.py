@@ -42,6 +42,9 @@ CASES = {
     "c1_singleview": (1, -1, -1, dict(mode=1, method=2, rank=60, rank2=121)),
     # C2: the config's own solver (Nystrom k = 40, p = 10), full 200-step window, all 5 GN iterations
     "c2_full": (2, -1, -1, dict(mode=1, method=1, rank=50)),
+    # C3: the config's own solver (RandSVD k = 100, p = 10: one block of 110 products per sketch) on the full
+    # 512^2 grid over an 8-step window (2 observation intervals), 2 GN iterations
+    "c3_w8": (3, 8, 4, dict(mode=1, method=0, rank=110, max_gn_iters=2)),
     # C4: the config's adaptive Nystrom (10 by 10 to 100, SketchPrecA with the reuse test) on the full
     # 256^2 grid over a 40-step window (2 intervals), 3 GN iterations so the reuse decision is taken twice
     "c4_w40": (4, 40, 20, dict(mode=2, method=1, rank=10, growth=10, max_rank=100, rank2=201, max_gn_iters=3)),
