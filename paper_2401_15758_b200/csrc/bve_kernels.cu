@@ -1208,6 +1208,15 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
 #pragma unroll
       for (int o = 0; o < T; ++o) out[static_cast<long long>(o) * (N / 2)] = w[o];
     }
+    if constexpr (MODE == kModeTlm) {
+      // fused observation gather (stage 3 at an interval end): this CTA wrote
+      // the new state of its own rows in sweep B
+      if (stage == 3 && p.obs_y) {
+        __syncthreads();
+        const int o0 = p.obs_tile[blockIdx.x], o1 = p.obs_tile[blockIdx.x + 1];
+        for (int o = o0 + tid; o < o1; o += kThreads) p.obs_y[v * p.obs_m + o] = p.d[off + p.obs_idx[o]] * p.obs_w[o];
+      }
+    }
     return;
   }
 #pragma unroll 1

@@ -52,6 +52,16 @@ struct StageArgs {
   const double2* car_e = nullptr;
   double2* lsum = nullptr;
   const double4* stab = nullptr;
+  // Observation gather fused into the fused TLM stage-3 launch at an
+  // interval end (proj/src/fourdvar.cpp:145-160: y_i = R_i^{-1/2} O x_i):
+  // obs_y[v * obs_m + o] = d[v][obs_idx[o]] * obs_w[o] for the observations
+  // o in [obs_tile[q], obs_tile[q + 1]) of the CTA's 8-row tile q (indices
+  // sorted). obs_y == nullptr: no gather.
+  const long long* obs_idx = nullptr;
+  const double* obs_w = nullptr;
+  double* obs_y = nullptr;
+  const int* obs_tile = nullptr;
+  long long obs_m = 0;
   double dt = 0, nu = 0, inv12h2 = 0, invh2 = 0;
 };
 

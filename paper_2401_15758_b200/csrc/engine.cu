@@ -10,6 +10,7 @@
 //   Problem::gram_apply     <- GramMap::apply (include/sketchdav/linalg.hpp:72-74)
 //   Problem::evaluate       <- evaluate (src/fourdvar.cpp:92-132), control-variable background term
 //   Problem::prior_sqrt     <- PriorCovariance::apply_sqrt (src/prior.cpp:64-69), Fourier-diagonal B
+#include <algorithm>
 #include <cmath>
 #include <map>
 #include <cstdlib>
@@ -135,6 +136,14 @@ Problem::Problem(const ProblemDesc& d, long long n_obs, const long long* idx, co
   rinv_.upload(m > 0 ? ri.data() : &zero, static_cast<size_t>(std::max<long long>(m, 1)), st_);
   background_.upload(background, static_cast<size_t>(dim_), st_);
   const int n = d.n;
+  if (d.model == kModelBVE && n_obs > 0 && n % 8 == 0 && std::is_sorted(idx, idx + n_obs)) {
+    // observations per 8-row tile for the gather fused into the TLM stage kernel
+    const int q = n / 8;
+    std::vector<int> tile(static_cast<size_t>(q) + 1);
+    for (int t = 0; t <= q; ++t)
+      tile[t] = static_cast<int>(std::lower_bound(idx, idx + n_obs, static_cast<long long>(t) * 8 * n) - idx);
+    obs_tile_.upload(tile.data(), tile.size(), st_);
+  }
   if (d.model == kModelBVE3) {
     // proj/src/bve.cpp:12-26: dx = 1/(nx+1) on [0,1], dy = 2/(ny+1) on [-1,1]
     const double dx = 1.0 / (n + 1), dy = 2.0 / (d.ny + 1);
@@ -517,6 +526,14 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
           if (fz) {
             set_fused(a, L.woff);
             if (first) a.flags |= kFlagRawIn;
+            if (s == 3 && y && (k + 1) % d_.spi == 0 && obs_tile_.get() && !L.lite) {
+              const int iv = (k + 1) / d_.spi - 1;
+              a.obs_idx = idx_.get();
+              a.obs_w = w + static_cast<long long>(iv) * n_obs_;
+              a.obs_y = y + L.v0 * m() + static_cast<long long>(iv) * n_obs_;
+              a.obs_tile = obs_tile_.get();
+              a.obs_m = m();
+            }
           }
           if (L.lite) {
             set_fused(a, L.woff);
@@ -533,6 +550,7 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
       if (y && (k + 1) % d_.spi == 0) {
         const int iv = (k + 1) / d_.spi - 1;
         for (auto& L : lanes) {
+          if (L.fz && !L.lite && obs_tile_.get()) continue;  // gathered inside the stage-3 launch
           gather_obs(state + L.v0 * dim_, dim_, idx_.get(), static_cast<int>(n_obs_),
                      w + static_cast<long long>(iv) * n_obs_, y + L.v0 * m() + static_cast<long long>(iv) * n_obs_,
                      m(), L.cnt, L.st);

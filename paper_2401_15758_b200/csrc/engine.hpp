@@ -105,6 +105,7 @@ class Problem {
   long long dim_ = 0, n_obs_ = 0;
   cudaStream_t st_ = nullptr;
   DevBuf<long long> idx_;
+  DevBuf<int> obs_tile_;  // BVE, sorted indices: first observation of each 8-row tile (fused gather)
   DevBuf<double> values_, rinv_sqrt_, rinv_, background_;
   DevBuf<double> sym_b_, sym_p_;
   DevBuf<double> solve_tab_;  // BVE: per-kx recurrence constants of the Poisson column solve
