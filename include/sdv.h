@@ -153,6 +153,11 @@ int sdv_thin_qr(sdv_problem* p, int64_t n, int64_t l, const double* y, double* q
 int sdv_thin_qr_dev(sdv_problem* p, int64_t n, int64_t l, double* y_dev, double* r, int* ndef);
 int sdv_evd_from_tall_dev(sdv_problem* p, int64_t n, int64_t l, double* wt_dev, double shift, int floor0,
                           double* basis_dev, double* eig);
+/* Nystrom tail (nystrom_assemble, proj/src/sketch.cpp:162-200) from device
+ * Omega and Y = H Omega (n x l each): basis (device n x l, may be NULL) and
+ * eigenvalues max(0, sigma^2 - nu). */
+int sdv_nystrom_assemble_dev(sdv_problem* p, int64_t n, int64_t l, const double* omega_dev, const double* y_dev,
+                             double* basis_dev, double* eig);
 
 /* Sketch of the misfit Hessian at trajectory t (randsvd_sketch,
  * nystrom_sketch, singleview_sketch, lanczos_sketch; proj/src/sketch.cpp).

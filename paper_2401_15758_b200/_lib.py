@@ -85,6 +85,7 @@ def lib():
         "sdv_thin_qr": (C.c_int, [vp, C.c_int64, C.c_int64, D, D, D, I32]),
         "sdv_thin_qr_dev": (C.c_int, [vp, C.c_int64, C.c_int64, vp, D, I32]),
         "sdv_evd_from_tall_dev": (C.c_int, [vp, C.c_int64, C.c_int64, vp, C.c_double, C.c_int, vp, D]),
+        "sdv_nystrom_assemble_dev": (C.c_int, [vp, C.c_int64, C.c_int64, vp, vp, vp, D]),
         "sdv_sketch": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_uint64, D, D, I64]),
         "sdv_lanczos_sketch": (C.c_int, [vp, C.c_int, D, D, D, I64]),
         "sdv_pcg_solve": (C.c_int, [vp, D, C.c_int64, D, D, C.c_double, C.c_int, D, I32]),

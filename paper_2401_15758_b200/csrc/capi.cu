@@ -354,6 +354,25 @@ int sdv_evd_from_tall_dev(sdv_problem* p, int64_t n, int64_t l, double* wt_dev, 
   });
 }
 
+int sdv_nystrom_assemble_dev(sdv_problem* p, int64_t n, int64_t l, const double* omega_dev, const double* y_dev,
+                             double* basis_dev, double* eig) {
+  return guard([&] {
+    need(p, "problem");
+    need(omega_dev, "omega");
+    need(y_dev, "y");
+    need(eig, "eig");
+    if (n < 1 || l < 1 || l > n) throw std::invalid_argument("nystrom_assemble: need 1 <= l <= n");
+    Lock lk(p->mu);
+    cudaStream_t st = p->p->stream();
+    sdv::DeviceEVD e = sdv::nystrom_assemble(omega_dev, y_dev, n, static_cast<int>(l), st);
+    const size_t nl = static_cast<size_t>(n) * static_cast<size_t>(l);
+    if (basis_dev)
+      SDV_CUDA(cudaMemcpyAsync(basis_dev, e.basis.get(), sizeof(double) * nl, cudaMemcpyDeviceToDevice, st));
+    SDV_CUDA(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < l; ++i) eig[i] = e.eig[static_cast<size_t>(i)];
+  });
+}
+
 int sdv_sketch(sdv_traj* t, int method, int rank, int rank2, uint64_t seed, double* eig, double* basis,
                int64_t counts[3]) {
   return guard([&] {

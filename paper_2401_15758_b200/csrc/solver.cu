@@ -187,7 +187,6 @@ SketchResult randsvd_sketch(MisfitOp& a, int rank, uint64_t seed) {
   return res;
 }
 
-namespace {
 // Stabilised Nystrom assembly (proj/src/sketch.cpp:162-200).
 DeviceEVD nystrom_assemble(const double* omega, const double* y, long long n, int l, cudaStream_t st) {
   DevBuf<double> tmp(static_cast<size_t>(n) * l);
@@ -236,7 +235,6 @@ DeviceEVD nystrom_assemble(const double* omega, const double* y, long long n, in
   }
   throw std::logic_error("nystrom_assemble: unreachable");
 }
-}  // namespace
 
 // proj/src/sketch.cpp:202-220 (h = GramMap, one H-apply = 1 TLM + 1 ADJ).
 SketchResult nystrom_sketch(MisfitOp& h, int rank, uint64_t seed) {

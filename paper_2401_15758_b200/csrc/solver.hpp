@@ -26,6 +26,9 @@ struct DeviceEVD {
 // EVD of G^T G from its tall factor Wt = G^T (n x l, overwritten by its QR
 // factor): the RandSVD / Nystrom tail (proj/src/sketch.cpp:27-33, :191-197).
 DeviceEVD evd_from_tall(DevBuf<double>& wt, long long n, int l, double shift, bool floor0, cudaStream_t st);
+// Stabilised Nystrom assembly from Omega and Y = H Omega (n x l each, device;
+// proj/src/sketch.cpp:162-200).
+DeviceEVD nystrom_assemble(const double* omega, const double* y, long long n, int l, cudaStream_t st);
 
 // out = (I + V diag(lambda) V^T)^{-1} v (proj/src/linalg.cpp:32-50).
 void woodbury_apply(const DeviceEVD& e, const double* v, double* out, long long n, cudaStream_t st);

@@ -9,11 +9,14 @@ slice column_shard(l, world, r) and runs its columns as one device block
 (one block sweep per rank, every rank against its own copy of the same
 deterministic base trajectory).
 
-RandSVD (Algorithm 1) has two exchange steps, and these are the only
-collectives on the path:
+Nystrom (Algorithm 2, nystrom_sharded) has one exchange: Y = H Omega (n x l)
+is all-gathered and every rank runs the stabilised assembly. RandSVD
+(Algorithm 1) has two exchange steps, and these are the only collectives on
+its path:
   1. Y = A Omega (m x l): each rank holds the columns of its slice; an
      all-gather assembles Y, and every rank factorises the same Y with the same
-     device Householder QR (sdv_thin_qr_dev), so Q is replicated identically;
+     device QR (sdv_thin_qr_dev: CholQR2 / Householder), so Q is replicated
+     identically;
   2. W^T = A^T Q (n x l): each rank sweeps its slice of Q's columns; an
      all-gather assembles W^T and every rank runs the l x l tail
      (sdv_evd_from_tall_dev: QR of W^T, SVD of R), so the basis V_hat that PCG
@@ -146,8 +149,33 @@ class GpuSketchOps:
             self._sync_out()
         return z
 
+    def gram(self, V):
+        """H V = A^T A V (TLM + ADJ block sweeps): V host (k, n) -> device (k, n)."""
+        t = self.torch
+        v = t.as_tensor(np.ascontiguousarray(V), dtype=t.float64, device=self.device)
+        hv = t.empty_like(v)
+        if v.shape[0]:
+            self._sync_in()
+            check(lib().sdv_gram_apply_block_dev(self.traj.handle, C.c_void_p(v.data_ptr()), v.shape[0],
+                                                 C.c_void_p(hv.data_ptr())))
+            self._sync_out()
+        return hv
+
+    def nystrom_assemble(self, omega, Y):
+        """nystrom_assemble (proj/src/sketch.cpp:162-200) of host Omega (l, n) and device Y (l, n)."""
+        t = self.torch
+        l, n = Y.shape
+        om = t.as_tensor(np.ascontiguousarray(omega), dtype=t.float64, device=self.device)
+        eig = np.empty(l)
+        basis = t.empty((l, n), dtype=t.float64, device=self.device)
+        self._sync_in()
+        check(lib().sdv_nystrom_assemble_dev(self.problem.handle, n, l, C.c_void_p(om.data_ptr()),
+                                             C.c_void_p(Y.data_ptr()), C.c_void_p(basis.data_ptr()),
+                                             eig.ctypes.data_as(C.POINTER(C.c_double))))
+        return eig, basis
+
     def qr_(self, Y):
-        """In-place device Householder thin QR (proj/src/linalg.cpp:108-134): Y (l, m) -> Q."""
+        """In-place device thin QR (the sketches' QR, proj/src/linalg.cpp:108-134): Y (l, m) -> Q."""
         l, m = Y.shape
         r = np.empty((l, l))
         nd = C.c_int()
@@ -188,6 +216,24 @@ def randsvd_sharded(ops, rank, seed, comm=None):
     wt_local = ops.adjoint(q[lo:hi])  # this rank's ADJ sweeps
     wt = comm.allgather_rows(wt_local, widths)  # exchange 2: W^T (n x l)
     eig, basis = ops.evd_from_tall(wt)  # replicated tail -> V_hat on every rank
+    return eig, basis, {"tlm": rank, "adj": rank, "final_rank": rank, "columns": (lo, hi)}
+
+
+def nystrom_sharded(ops, rank, seed, comm=None):
+    """nystrom_sketch(H, rank, seed) (proj/src/sketch.cpp:202-220) with Omega's
+    columns sharded over comm's ranks: each rank applies H = A^T A to its
+    columns (one TLM + ADJ block sweep), Y = H Omega is all-gathered, and every
+    rank runs the same stabilised assembly (replicated basis)."""
+    if comm is None:
+        comm = TorchComm()
+    if rank < 1 or rank > ops.n:
+        raise ValueError("nystrom_sketch: need 1 <= rank <= n")
+    counts = [column_shard(rank, comm.world, r) for r in range(comm.world)]
+    widths = [hi - lo for lo, hi in counts]
+    lo, hi = counts[comm.rank]
+    omega = ops.gaussian(rank, seed)
+    y = comm.allgather_rows(ops.gram(omega[lo:hi]), widths)  # the one exchange: Y (n x l)
+    eig, basis = ops.nystrom_assemble(omega, y)
     return eig, basis, {"tlm": rank, "adj": rank, "final_rank": rank, "columns": (lo, hi)}
 
 

@@ -143,3 +143,26 @@ def test_sharded_randsvd_threads_on_gpu(oracle, sdv, cfg, steps, spi, l, world):
         otr = osc.linearize(osc.background)
         eo, _, _ = otr.sketch(0, l, seed, workers=max(2, os.cpu_count() or 2))
         assert eig_rel(e0, eo) <= 1e-8
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,steps,spi,l,world", [(0, -1, -1, 30, 2), (2, 20, -1, 50, 2), (1, -1, -1, 60, 4)])
+def test_sharded_nystrom_threads_on_gpu(oracle, sdv, cfg, steps, spi, l, world):
+    """Sharded Nystrom (one all-gather of Y = H Omega, replicated assembly) vs the single-process device
+    sketch (<= 1e-10) and the oracle (<= 1e-8): C0, C2's config sketch (k = 40, p = 10), C1 (k = 50, p = 10)."""
+    from test_gpu_parity import eig_rel, pair
+
+    osc, prob = pair(oracle, cfg, steps, spi)
+    gtr = prob.linearize(osc.background)
+    seed = oracle.mix_seed(2, 0x736b6574636800)
+    eg, _, _ = gtr.sketch(1, l, seed)
+    ops = sdist.GpuSketchOps(gtr)
+    outs = sdist.run_threads(world, lambda comm: sdist.nystrom_sharded(ops, l, seed, comm))
+    e0, b0, c0 = outs[0]
+    for e, b, c in outs[1:]:
+        assert np.array_equal(e, e0) and torch.equal(b, b0)
+    assert c0["tlm"] == l and c0["adj"] == l
+    assert eig_rel(e0, eg) <= 1e-10
+    otr = osc.linearize(osc.background)
+    eo, _, _ = otr.sketch(1, l, seed, workers=max(2, os.cpu_count() or 2))
+    assert eig_rel(e0, eo) <= 1e-8
