@@ -108,6 +108,28 @@ int sdv_forward(sdv_problem* p, const double* x0, int steps, double* out);
  * sweep storing every RK4 stage input on the device. */
 int sdv_linearize(sdv_problem* p, const double* x0, sdv_traj** out);
 int sdv_linearize_dev(sdv_problem* p, const double* x0_dev, sdv_traj** out);
+/* DynamicalModel::linearize(x0, steps, checkpoint_stride) with its stride
+ * (proj/include/sketchdav/model.hpp:36-40; the reference's checkpointed
+ * trajectory is proj/src/burgers.cpp:114-191). policy:
+ *   SDV_STORE_AUTO       every RK stage in HBM when it fits (the contract's
+ *                        "implementations may store more"), else checkpoints
+ *                        every min(checkpoint_stride, what fits) steps;
+ *   SDV_STORE_FULL       every RK stage (sdv_linearize);
+ *   SDV_STORE_CHECKPOINT states every checkpoint_stride (>= 1) steps; the
+ *                        sweeps recompute one segment of stage inputs at a
+ *                        time from its checkpoint (results bitwise equal to
+ *                        the full store).
+ * The Dirichlet BVE (SDV_MODEL_BVE_DIRICHLET) stores every stage whatever the
+ * policy, as the reference BVE (proj/src/bve.cpp:221-225). sdv_linearize is
+ * SDV_STORE_AUTO with the problem's steps per interval as the stride. */
+#define SDV_STORE_AUTO 0
+#define SDV_STORE_FULL 1
+#define SDV_STORE_CHECKPOINT 2
+int sdv_linearize_ex(sdv_problem* p, const double* x0, int checkpoint_stride, int policy, sdv_traj** out);
+int sdv_linearize_ex_dev(sdv_problem* p, const double* x0_dev, int checkpoint_stride, int policy, sdv_traj** out);
+/* info = {total_steps, checkpoint stride (0 = every stage stored), segments,
+ * bytes of HBM the trajectory holds} */
+int sdv_traj_info(const sdv_traj* t, int64_t info[4]);
 void sdv_traj_destroy(sdv_traj* t);
 /* LinearizedTrajectory::state_at / tlm_range / adj_range
  * (proj/include/sketchdav/model.hpp:17-21), batched over s vectors. */

@@ -22,6 +22,8 @@ from ._lib import D, GNConfigC, I32, I64, ProblemDesc, check, lib
 MODEL_BURGERS, MODEL_BVE, MODEL_BURGERS_DIRICHLET, MODEL_BVE_DIRICHLET = 1, 2, 3, 4
 PRIOR_FOURIER, PRIOR_LAPLACIAN = 0, 1
 RANDSVD, NYSTROM, SINGLEVIEW, LANCZOS = 0, 1, 2, 3
+# linearize storage policies (sdv.h SDV_STORE_*)
+STORE_AUTO, STORE_FULL, STORE_CHECKPOINT = 0, 1, 2
 MODES = {"SketchSolv": 0, "SketchPrec": 1, "SketchPrecA": 2, "PrecGamma": 3, "PrecLanczos": 4, "PrecALanczos": 5}
 
 
@@ -124,14 +126,28 @@ class Problem:
         check(lib().sdv_forward(self._h, _p(_f64(x0)), steps, _p(out)))
         return out
 
-    def linearize(self, x0):
+    def linearize(self, x0, checkpoint_stride=None, policy=None):
+        """DynamicalModel::linearize (model.hpp:36-40). With no stride: every
+        RK stage stored when it fits HBM (else checkpoints every
+        steps_per_interval steps). policy: STORE_AUTO / STORE_FULL /
+        STORE_CHECKPOINT (sdv.h)."""
         t = C.c_void_p()
-        check(lib().sdv_linearize(self._h, _p(_f64(x0)), C.byref(t)))
+        if checkpoint_stride is None and policy is None:
+            check(lib().sdv_linearize(self._h, _p(_f64(x0)), C.byref(t)))
+        else:
+            stride = self.spi if checkpoint_stride is None else int(checkpoint_stride)
+            pol = STORE_AUTO if policy is None else int(policy)
+            check(lib().sdv_linearize_ex(self._h, _p(_f64(x0)), stride, pol, C.byref(t)))
         return Trajectory(self, t)
 
-    def linearize_dev(self, x0_dev):
+    def linearize_dev(self, x0_dev, checkpoint_stride=None, policy=None):
         t = C.c_void_p()
-        check(lib().sdv_linearize_dev(self._h, C.c_void_p(x0_dev), C.byref(t)))
+        if checkpoint_stride is None and policy is None:
+            check(lib().sdv_linearize_dev(self._h, C.c_void_p(x0_dev), C.byref(t)))
+        else:
+            stride = self.spi if checkpoint_stride is None else int(checkpoint_stride)
+            pol = STORE_AUTO if policy is None else int(policy)
+            check(lib().sdv_linearize_ex_dev(self._h, C.c_void_p(x0_dev), stride, pol, C.byref(t)))
         return Trajectory(self, t)
 
     def prior_sqrt(self, V):
@@ -210,6 +226,12 @@ class Trajectory:
 
     def total_steps(self):
         return self.problem.total_steps
+
+    def info(self):
+        """{steps, stride (0 = every stage stored), segments, bytes}"""
+        v = (C.c_int64 * 4)()
+        check(lib().sdv_traj_info(self._h, v))
+        return {"steps": v[0], "stride": v[1], "segments": v[2], "bytes": v[3]}
 
     def state_at(self, step):
         out = np.empty(self.problem.n)

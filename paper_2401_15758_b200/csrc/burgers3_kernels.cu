@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(1024) burgers3_tlm_kernel(BurgersArgs p, doubl
 #pragma unroll
   for (int q = 0; q < NPT; ++q) D[q] = (tid + q * nt < n) ? state[v * n + tid + q * nt] : 0.0;
   for (int k = p.k0; k < p.k1; ++k) {
-    const double* u0 = p.base + static_cast<long long>(k) * 3 * n;
+    const double* u0 = p.base + static_cast<long long>(k - p.base_k0) * 3 * n;
     const double* u1 = u0 + n;
     const double* u2 = u0 + 2 * n;
 #pragma unroll
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(1024) burgers3_adj_kernel(BurgersArgs p, doubl
                        p.w[static_cast<long long>(iv) * p.n_obs + o];
       __syncthreads();
     }
-    const double* u0 = p.base + static_cast<long long>(k) * 3 * n;
+    const double* u0 = p.base + static_cast<long long>(k - p.base_k0) * 3 * n;
     const double* u1 = u0 + n;
     const double* u2 = u0 + 2 * n;
     double T2[NPT], T1[NPT];

@@ -107,13 +107,13 @@ __global__ void __launch_bounds__(1024) burgers_tlm_kernel(BurgersArgs p, double
     sh[tid + q * nt] = D[q];
   }
   __syncthreads();
-  if (tid == 0 && t0 < t1) br.issue(p.base + t0 * n, n, 0);
+  if (tid == 0 && t0 < t1) br.issue(p.base + (t0 - 4LL * p.base_k0) * n, n, 0);
   for (int k = p.k0; k < p.k1; ++k) {
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const long long t = static_cast<long long>(k) * 4 + s;
       const int slot = static_cast<int>((t - t0) & 1);
-      if (tid == 0 && t + 1 < t1) br.issue(p.base + (t + 1) * n, n, slot ^ 1);
+      if (tid == 0 && t + 1 < t1) br.issue(p.base + (t + 1 - 4LL * p.base_k0) * n, n, slot ^ 1);
       const double* u = br.wait(slot);
       const double* X = sh + cur * n;
       double* Xn = sh + (cur ^ 1) * n;
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(1024) burgers_adj_kernel(BurgersArgs p, double
 #pragma unroll
   for (int q = 0; q < NPT; ++q) L[q] = state[v * n + tid + q * nt];
   __syncthreads();
-  if (tid == 0 && tfirst <= tlast) br.issue(p.base + tlast * n, n, 0);
+  if (tid == 0 && tfirst <= tlast) br.issue(p.base + (tlast - 4LL * p.base_k0) * n, n, 0);
   int cur = 0;
   for (int k = p.k1 - 1; k >= p.k0; --k) {
     if (p.y && (k + 1) % p.spi == 0) {
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(1024) burgers_adj_kernel(BurgersArgs p, double
       }
       const double* u = br.wait(slot);
       __syncthreads();  // also: every thread is past the previous stage's reads of the other base row
-      if (tid == 0 && t - 1 >= tfirst) br.issue(p.base + (t - 1) * n, n, slot ^ 1);
+      if (tid == 0 && t - 1 >= tfirst) br.issue(p.base + (t - 1 - 4LL * p.base_k0) * n, n, slot ^ 1);
 #pragma unroll
       for (int q = 0; q < NPT; ++q) {
         const int i = tid + q * nt, im = wrapm(i - 1, n), ip = wrapm(i + 1, n);

@@ -10,6 +10,7 @@ struct BurgersArgs {
   double dt = 0, nu = 0, c1 = 0, c2 = 0;  // c1 = 1/(2 dx), c2 = 1/dx^2
   const double* base = nullptr;           // [steps][4][n] stage inputs
   int k0 = 0, k1 = 0;                     // step range
+  int base_k0 = 0;                        // step of base's first row block (checkpoint segments)
   // observation gather/scatter (enabled when y != nullptr)
   const long long* idx = nullptr;
   int n_obs = 0;

@@ -157,6 +157,44 @@ int sdv_forward(sdv_problem* p, const double* x0, int steps, double* out) {
   });
 }
 
+int sdv_linearize_ex_dev(sdv_problem* p, const double* x0_dev, int checkpoint_stride, int policy, sdv_traj** out) {
+  return guard([&] {
+    need(p, "problem");
+    Lock lk(p->mu);
+    need(x0_dev, "x0");
+    need(out, "out");
+    auto t = std::make_unique<sdv_traj>();
+    t->owner = p;
+    t->t = p->p->linearize(x0_dev, checkpoint_stride, policy);
+    *out = t.release();
+  });
+}
+int sdv_linearize_ex(sdv_problem* p, const double* x0, int checkpoint_stride, int policy, sdv_traj** out) {
+  return guard([&] {
+    need(p, "problem");
+    Lock lk(p->mu);
+    need(x0, "x0");
+    need(out, "out");
+    auto& q = *p->p;
+    sdv::DevBuf<double> d;
+    d.upload(x0, static_cast<size_t>(q.dim()), q.stream());
+    auto t = std::make_unique<sdv_traj>();
+    t->owner = p;
+    t->t = q.linearize(d.get(), checkpoint_stride, policy);
+    *out = t.release();
+  });
+}
+int sdv_traj_info(const sdv_traj* t, int64_t info[4]) {
+  return guard([&] {
+    need(t, "trajectory");
+    need(info, "info");
+    Lock lk(t->owner->mu);
+    info[0] = t->t->steps;
+    info[1] = t->t->stride;
+    info[2] = t->t->segments();
+    info[3] = static_cast<int64_t>(t->t->stored_bytes());
+  });
+}
 int sdv_linearize_dev(sdv_problem* p, const double* x0_dev, sdv_traj** out) {
   return guard([&] {
     need(p, "problem");
@@ -164,7 +202,7 @@ int sdv_linearize_dev(sdv_problem* p, const double* x0_dev, sdv_traj** out) {
     need(out, "out");
     auto t = std::make_unique<sdv_traj>();
     t->owner = p;
-    t->t = p->p->linearize(x0_dev);
+    t->t = p->p->linearize(x0_dev, p->p->desc().spi, sdv::kStoreAuto);
     *out = t.release();
   });
 }
@@ -178,7 +216,7 @@ int sdv_linearize(sdv_problem* p, const double* x0, sdv_traj** out) {
     d.upload(x0, static_cast<size_t>(q.dim()), q.stream());
     auto t = std::make_unique<sdv_traj>();
     t->owner = p;
-    t->t = q.linearize(d.get());
+    t->t = q.linearize(d.get(), q.desc().spi, sdv::kStoreAuto);
     *out = t.release();
   });
 }

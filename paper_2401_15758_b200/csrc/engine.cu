@@ -280,7 +280,15 @@ void Problem::ensure_work(int nvec) const {
 const double* Trajectory::state_at(int step) const {
   if (step < 0 || step > steps) throw std::invalid_argument("trajectory: step out of range");
   if (step == steps) return final.get();
-  return w.get() + static_cast<long long>(step) * stages * prob->dim();
+  if (!checkpointed()) return w.get() + static_cast<long long>(step) * stages * prob->dim();
+  // checkpoint mode (proj/src/burgers.cpp:142-150): the floor checkpoint,
+  // integrated forward to `step` when it is not one itself
+  const int j = step / stride;
+  const double* c = ckpt.get() + static_cast<long long>(j) * prob->dim();
+  if (step == j * stride) return c;
+  scratch.ensure(static_cast<size_t>(prob->dim()));
+  prob->forward(c, step - j * stride, scratch.get());
+  return scratch.get();
 }
 
 namespace {
@@ -338,14 +346,20 @@ void Problem::forward(const double* d_x0, int steps, double* d_out) const {
     return;
   }
   ensure_work(1);
+  if (d_out != d_x0) SDV_CUDA(cudaMemcpyAsync(d_out, d_x0, sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
+  bve_nl(d_out, steps, nullptr, nullptr, NlWork{wx0_.get(), wx1_.get(), wa_.get(), ws0_.get(), ws1_.get()});
+}
+
+// Periodic BVE NL forward (RK4 stages of NL-mode stage_kernel, column Poisson
+// pass), u in/out; stores every stage input / streamfunction when store_w is
+// set ([steps][4][dim] from store_w / store_p).
+void Problem::bve_nl(double* u, int steps, double* store_w, double* store_p, const NlWork& wk) const {
   const int n = d_.n;
-  double* u = d_out;
-  if (u != d_x0) SDV_CUDA(cudaMemcpyAsync(u, d_x0, sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
-  double2* s_cur = ws0_.get();
-  double2* s_nxt = ws1_.get();
+  double2* s_cur = wk.s0;
+  double2* s_nxt = wk.s1;
   bve_row_fwd(n, u, s_cur, 1, st_);
   count_launch();
-  double* xb[2] = {wx0_.get(), wx1_.get()};
+  double* xb[2] = {wk.x0, wk.x1};
   for (int k = 0; k < steps; ++k)
     for (int s = 0; s < 4; ++s) {
       poisson_col(s_cur, 1, st_);
@@ -356,18 +370,48 @@ void Problem::forward(const double* d_x0, int steps, double* d_out) const {
       a.x_in = s == 0 ? u : xb[(s - 1) & 1];
       a.x_out = s < 3 ? xb[s & 1] : nullptr;
       a.d = u;
-      a.acc = wa_.get();
+      a.acc = wk.acc;
+      if (store_w) {
+        a.store_w = store_w + (static_cast<long long>(k) * 4 + s) * dim_;
+        a.store_p = store_p + (static_cast<long long>(k) * 4 + s) * dim_;
+      }
       bve_stage(n, kModeNl, a, 1, st_);
       count_launch();
       std::swap(s_cur, s_nxt);
     }
 }
 
-std::unique_ptr<Trajectory> Problem::linearize(const double* d_x0) const {
+std::unique_ptr<Trajectory> Problem::linearize(const double* d_x0, int stride, int policy) const {
+  if (policy != kStoreAuto && policy != kStoreFull && policy != kStoreCheckpoint)
+    throw std::invalid_argument("linearize: unknown storage policy");
+  if (policy == kStoreCheckpoint && stride < 1) throw std::invalid_argument("linearize: checkpoint stride must be >= 1");
   auto tr = std::make_unique<Trajectory>();
   tr->prob = this;
   tr->steps = total_steps();
   tr->stages = (d_.model == kModelBurgers3 || d_.model == kModelBVE3) ? 3 : 4;
+  const int fields = (d_.model == kModelBVE || d_.model == kModelBVE3) ? 2 : 1;
+  // The reference BVE stores every stage whatever the stride
+  // (proj/src/bve.cpp:221-225); the Dirichlet BVE here does the same.
+  if (d_.model != kModelBVE3 && tr->steps > 1) {
+    if (policy == kStoreAuto) {
+      size_t free_b = 0, total_b = 0;
+      SDV_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const double full = 8.0 * fields * tr->stages * static_cast<double>(dim_) * tr->steps;
+      if (full > 0.75 * static_cast<double>(free_b)) {
+        // largest segment that leaves half the free memory to the sweeps
+        const double seg_step = 8.0 * fields * tr->stages * static_cast<double>(dim_);
+        const int fit = static_cast<int>(std::max(1.0, 0.5 * static_cast<double>(free_b) / seg_step - 1.0));
+        tr->stride = std::min(tr->steps, std::max(1, stride > 0 ? std::min(stride, fit) : fit));
+      }
+    } else if (policy == kStoreCheckpoint) {
+      tr->stride = std::min(stride, tr->steps);
+    }
+    if (tr->stride >= tr->steps && policy != kStoreCheckpoint) tr->stride = 0;
+  }
+  if (tr->checkpointed()) {
+    linearize_ckpt(*tr, d_x0);
+    return tr;
+  }
   const long long st_elems = static_cast<long long>(tr->steps) * tr->stages * dim_;
   tr->w.alloc(static_cast<size_t>(st_elems));
   tr->final.alloc(static_cast<size_t>(dim_));
@@ -398,42 +442,76 @@ std::unique_ptr<Trajectory> Problem::linearize(const double* d_x0) const {
   } else {
     tr->p.alloc(static_cast<size_t>(st_elems));
     ensure_work(1);
-    const int n = d_.n;
     double* u = tr->final.get();
     SDV_CUDA(cudaMemcpyAsync(u, d_x0, sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
-    double2* s_cur = ws0_.get();
-    double2* s_nxt = ws1_.get();
-    bve_row_fwd(n, u, s_cur, 1, st_);
-    count_launch();
-    double* xb[2] = {wx0_.get(), wx1_.get()};
-    for (int k = 0; k < tr->steps; ++k)
-      for (int s = 0; s < 4; ++s) {
-        poisson_col(s_cur, 1, st_);
-        StageArgs a = bve_args(d_);
-        a.stage = s;
-        a.s_in = s_cur;
-        a.s_out = s_nxt;
-        a.x_in = s == 0 ? u : xb[(s - 1) & 1];
-        a.x_out = s < 3 ? xb[s & 1] : nullptr;
-        a.d = u;
-        a.acc = wa_.get();
-        a.store_w = tr->w.get() + (static_cast<long long>(k) * 4 + s) * dim_;
-        a.store_p = tr->p.get() + (static_cast<long long>(k) * 4 + s) * dim_;
-        bve_stage(n, kModeNl, a, 1, st_);
-        count_launch();
-        std::swap(s_cur, s_nxt);
-      }
+    bve_nl(u, tr->steps, tr->w.get(), tr->p.get(), NlWork{wx0_.get(), wx1_.get(), wa_.get(), ws0_.get(), ws1_.get()});
   }
-  // Non-finite check on the final state (reference throws on NaN/Inf,
-  // proj/src/burgers.cpp:128-131, proj/src/bve.cpp:120-124).
+  check_final(*tr);
+  return tr;
+}
+
+// Non-finite check on the final state (reference throws on NaN/Inf,
+// proj/src/burgers.cpp:128-131, proj/src/bve.cpp:120-124).
+void Problem::check_final(const Trajectory& tr) const {
   DevBuf<double> r(1);
-  dev_dot(tr->final.get(), tr->final.get(), dim_, r.get(), st_);
+  dev_dot(tr.final.get(), tr.final.get(), dim_, r.get(), st_);
   double nn = 0.0;
   SDV_CUDA(cudaMemcpyAsync(&nn, r.get(), sizeof(double), cudaMemcpyDeviceToHost, st_));
   SDV_CUDA(cudaStreamSynchronize(st_));
   if (!std::isfinite(nn))
     throw std::runtime_error("linearize: non-finite state (time step too large for stability)");
-  return tr;
+}
+
+// Checkpoint-mode linearize (proj/src/burgers.cpp:114-138): the states at
+// multiples of the stride, one segment buffer of stage inputs (left holding
+// the last segment).
+void Problem::linearize_ckpt(Trajectory& tr, const double* d_x0) const {
+  const int nseg = tr.segments();
+  const long long seg_elems = static_cast<long long>(tr.stride) * tr.stages * dim_;
+  tr.w.alloc(static_cast<size_t>(seg_elems));
+  if (d_.model == kModelBVE) tr.p.alloc(static_cast<size_t>(seg_elems));
+  tr.ckpt.alloc(static_cast<size_t>(nseg) * dim_);
+  tr.final.alloc(static_cast<size_t>(dim_));
+  SDV_CUDA(cudaMemcpyAsync(tr.ckpt.get(), d_x0, sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
+  for (int j = 0; j < nseg; ++j) {
+    tr.seg = -1;
+    fill_segment(tr, j);
+    // the segment's end state: the next checkpoint, or the final state
+    double* nxt = j + 1 < nseg ? tr.ckpt.get() + static_cast<long long>(j + 1) * dim_ : tr.final.get();
+    const double* end = d_.model == kModelBVE ? tr.ru.get() : tr.scratch.get();
+    SDV_CUDA(cudaMemcpyAsync(nxt, end, sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
+  }
+  check_final(tr);
+}
+
+// Recompute segment j's stage inputs from its checkpoint into tr.w / tr.p; the
+// segment's end state is left in tr.ru (BVE) / tr.scratch (Burgers).
+void Problem::fill_segment(const Trajectory& tr, int j) const {
+  const int k0 = j * tr.stride, len = std::min(tr.stride, tr.steps - k0);
+  const double* c = tr.ckpt.get() + static_cast<long long>(j) * dim_;
+  if (d_.model == kModelBVE) {
+    const size_t f = static_cast<size_t>(dim_), sp = static_cast<size_t>(d_.n) * (d_.n / 2);
+    tr.ru.ensure(f);
+    tr.rx0.ensure(f);
+    tr.rx1.ensure(f);
+    tr.racc.ensure(f);
+    tr.rs0.ensure(sp);
+    tr.rs1.ensure(sp);
+    SDV_CUDA(cudaMemcpyAsync(tr.ru.get(), c, sizeof(double) * dim_, cudaMemcpyDeviceToDevice, st_));
+    bve_nl(tr.ru.get(), len, tr.w.get(), tr.p.get(), NlWork{tr.rx0.get(), tr.rx1.get(), tr.racc.get(), tr.rs0.get(), tr.rs1.get()});
+  } else {
+    tr.scratch.ensure(static_cast<size_t>(dim_));
+    if (d_.model == kModelBurgers3) burgers3_fwd(burgers_args(d_), c, tr.w.get(), tr.scratch.get(), len, st_);
+    else burgers_fwd(burgers_args(d_), c, tr.w.get(), tr.scratch.get(), len, st_);
+    count_launch();
+  }
+  tr.seg = j;
+}
+
+void Problem::hold_segment(const Trajectory& tr, int k) const {
+  if (!tr.checkpointed()) return;
+  const int j = k / tr.stride;
+  if (j != tr.seg) fill_segment(tr, j);
 }
 
 void Problem::prior_sqrt(const double* in, double* out, int nvec) const {
@@ -479,15 +557,26 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
     a.w = w;
     a.y = y;
     a.m = m();
-    if (d_.model == kModelBurgers3)
-      burgers3_tlm(a, state, nvec, st_);
-    else
-      burgers_tlm(a, state, nvec, st_);
-    count_launch();
-    count_path(kPathBurgers);
+    // checkpoint mode: one launch per segment, in step order
+    const int step = tr.checkpointed() ? tr.stride : k1 - k0;
+    if (tr.checkpointed()) tr.seg = -1;
+    for (int ka = tr.checkpointed() ? (k0 / step) * step : k0; ka < k1; ka += step) {
+      a.k0 = std::max(k0, ka);
+      a.k1 = std::min(k1, ka + step);
+      hold_segment(tr, a.k0);
+      a.base = tr.w.get();
+      a.base_k0 = tr.held_k0();
+      if (d_.model == kModelBurgers3)
+        burgers3_tlm(a, state, nvec, st_);
+      else
+        burgers_tlm(a, state, nvec, st_);
+      count_launch();
+      count_path(kPathBurgers);
+    }
     return;
   }
   ensure_work(nvec);
+  if (tr.checkpointed()) tr.seg = -1;  // each sweep recomputes what it reads (graph replays stay valid)
   const int n = d_.n, g = std::min(nvec, group());
   const long long sdim = static_cast<long long>(n) * (n / 2);
   for (int v0 = 0; v0 < nvec; v0 += g) {
@@ -501,6 +590,12 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
     }
     bool first = true;
     for (int k = k0; k < k1; ++k) {
+      if (tr.checkpointed() && k / tr.stride != tr.seg) {
+        // the lanes finish the held segment before it is overwritten
+        join_lanes(lanes);
+        hold_segment(tr, k);
+        refork_lanes(lanes);
+      }
       for (int s = 0; s < 4; ++s) {
         // interleave the lanes' launches so their kernels co-reside on SMs;
         // fused lanes: the first stage reads column-solved spectra, later
@@ -521,8 +616,8 @@ void Problem::tlm(const Trajectory& tr, double* state, int nvec, int k0, int k1,
           a.x_out = s < 3 ? xb[s & 1] : nullptr;
           a.d = dst;
           a.acc = wa_.get() + L.woff * dim_;
-          a.base_w = tr.w.get() + (static_cast<long long>(k) * 4 + s) * dim_;
-          a.base_p = tr.p.get() + (static_cast<long long>(k) * 4 + s) * dim_;
+          a.base_w = tr.base_w(k, s, dim_);
+          a.base_p = tr.base_p(k, s, dim_);
           if (fz) {
             set_fused(a, L.woff);
             if (first) a.flags |= kFlagRawIn;
@@ -603,6 +698,12 @@ std::vector<Problem::Lane> Problem::split_lanes(int v0, int gn) const {
   return lanes;
 }
 
+void Problem::refork_lanes(const std::vector<Lane>& lanes) const {
+  if (lanes.size() < 2) return;
+  SDV_CUDA(cudaEventRecord(ev_fork_, st_));
+  for (size_t i = 1; i < lanes.size(); ++i) SDV_CUDA(cudaStreamWaitEvent(lanes[i].st, ev_fork_, 0));
+}
+
 void Problem::join_lanes(const std::vector<Lane>& lanes) const {
   for (size_t i = 1; i < lanes.size(); ++i) {
     SDV_CUDA(cudaEventRecord(lane_ev_[i - 1], lanes[i].st));
@@ -625,15 +726,34 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
     a.w = w;
     a.y = const_cast<double*>(y);
     a.m = m();
-    if (d_.model == kModelBurgers3)
-      burgers3_adj(a, state, nvec, st_);
-    else
-      burgers_adj(a, state, nvec, st_);
-    count_launch();
-    count_path(kPathBurgers);
+    // checkpoint mode: one launch per segment, in reverse step order
+    if (!tr.checkpointed()) {
+      if (d_.model == kModelBurgers3)
+        burgers3_adj(a, state, nvec, st_);
+      else
+        burgers_adj(a, state, nvec, st_);
+      count_launch();
+      count_path(kPathBurgers);
+      return;
+    }
+    tr.seg = -1;
+    for (int kb = ((k1 - 1) / tr.stride) * tr.stride; kb + tr.stride > k0 && kb >= 0; kb -= tr.stride) {
+      a.k0 = std::max(k0, kb);
+      a.k1 = std::min(k1, kb + tr.stride);
+      hold_segment(tr, a.k0);
+      a.base = tr.w.get();
+      a.base_k0 = tr.held_k0();
+      if (d_.model == kModelBurgers3)
+        burgers3_adj(a, state, nvec, st_);
+      else
+        burgers_adj(a, state, nvec, st_);
+      count_launch();
+      count_path(kPathBurgers);
+    }
     return;
   }
   ensure_work(nvec);
+  if (tr.checkpointed()) tr.seg = -1;  // each sweep recomputes what it reads (graph replays stay valid)
   const int n = d_.n, g = std::min(nvec, group());
   const long long sdim = static_cast<long long>(n) * (n / 2);
   for (int v0 = 0; v0 < nvec; v0 += g) {
@@ -646,6 +766,11 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
     int qi = 0;
     bool first = true;
     for (int k = k1 - 1; k >= k0; --k) {
+      if (tr.checkpointed() && k / tr.stride != tr.seg) {
+        join_lanes(lanes);
+        hold_segment(tr, k);
+        refork_lanes(lanes);
+      }
       if (y && (k + 1) % d_.spi == 0) {
         const int iv = (k + 1) / d_.spi - 1;
         for (auto& L : lanes) {
@@ -675,8 +800,8 @@ void Problem::adj(const Trajectory& tr, double* state, int nvec, int k0, int k1,
           a.acc = wa_.get() + L.woff * dim_;
           a.q_in = (qi ? wx1_.get() : wx0_.get()) + L.woff * dim_;
           a.q_out = (qi ? wx0_.get() : wx1_.get()) + L.woff * dim_;
-          a.base_w = tr.w.get() + (static_cast<long long>(k) * 4 + s) * dim_;
-          a.base_p = tr.p.get() + (static_cast<long long>(k) * 4 + s) * dim_;
+          a.base_w = tr.base_w(k, s, dim_);
+          a.base_p = tr.base_p(k, s, dim_);
           if (fz) set_fused(a, L.woff);
           if (L.lite) {
             set_fused(a, L.woff);
@@ -740,7 +865,7 @@ void Problem::probe_adj_stage_kernels(const Trajectory& tr, int s, int stages, f
   double tot_stage = 0.0, tot_col = 0.0;
   int qi = 0;
   for (int q = 0; q < stages; ++q) {
-    const int k = tr.steps - 1 - (q / 4) % tr.steps, sg = 3 - q % 4;
+    const int k = tr.held_steps() - 1 - (q / 4) % tr.held_steps(), sg = 3 - q % 4;
     const bool has_prev = q > 0;
     SDV_CUDA(cudaEventRecord(ev[0], st_));
     if (has_prev) {
@@ -787,7 +912,7 @@ void Problem::probe_stage_kernels(const Trajectory& tr, int s, int stages, float
                              st_));
   double tot_stage = 0.0, tot_col = 0.0;
   if (d_.model == kModelBurgers || d_.model == kModelBurgers3) {
-    const int steps = std::max(1, std::min(tr.steps, stages / tr.stages));
+    const int steps = std::max(1, std::min(tr.held_steps(), stages / tr.stages));
     BurgersArgs a = burgers_args(d_);
     a.base = tr.w.get();
     a.k0 = 0;
@@ -814,7 +939,7 @@ void Problem::probe_stage_kernels(const Trajectory& tr, int s, int stages, float
     bve_row_fwd(n, dst, s_cur, s, st_);
     const bool fz = fused(s);
     for (int q = 0; q < stages; ++q) {
-      const int k = (q / 4) % tr.steps, sg = q % 4;
+      const int k = (q / 4) % tr.held_steps(), sg = q % 4;
       SDV_CUDA(cudaEventRecord(ev[0], st_));
       if (fz && q > 0) poisson_carry(s_cur, 0, s, st_);
       else poisson_col(s_cur, s, st_);

@@ -6,6 +6,7 @@
 // block (s-vector) device entry points.
 #pragma once
 
+#include <algorithm>
 #include <memory>
 
 #include "bve3_kernels.cuh"
@@ -38,15 +39,46 @@ struct ProblemDesc {
 
 class Problem;
 
+// Storage policy of linearize (DynamicalModel::linearize's checkpoint_stride,
+// proj/include/sketchdav/model.hpp:36-40): kStoreAuto keeps every RK stage in
+// HBM when that fits the device (the contract's "implementations may store
+// more") and falls back to checkpoints otherwise; kStoreCheckpoint always
+// stores states every `stride` steps and recomputes one segment of stage
+// inputs at a time inside the sweeps (proj/src/burgers.cpp:114-191).
+enum StorePolicy { kStoreAuto = 0, kStoreFull = 1, kStoreCheckpoint = 2 };
+
 // Device-resident base trajectory (FWD sweep output).
 struct Trajectory {
   const Problem* prob = nullptr;
   int steps = 0;
   int stages = 4;        // stored stage inputs per step (RK4: 4, RK3-TVD: 3)
-  DevBuf<double> w;      // [steps][4][dim] stage inputs
-  DevBuf<double> p;      // BVE: [steps][4][dim] stage streamfunctions
+  DevBuf<double> w;      // [steps][4][dim] stage inputs (checkpoint mode: one segment, [stride][4][dim])
+  DevBuf<double> p;      // BVE: [steps][4][dim] stage streamfunctions (checkpoint mode: one segment)
   DevBuf<double> final;  // [dim]
+  // Checkpoint mode (stride > 0): ckpt[j] = state at step j*stride; w/p hold
+  // the stage inputs of segment `seg` (steps [seg*stride, min(steps, (seg+1)*stride))).
+  int stride = 0;
+  DevBuf<double> ckpt;                  // [segments][dim]
+  mutable int seg = -1;                 // segment held in w/p (-1: none)
+  mutable DevBuf<double> scratch;       // state_at between checkpoints
+  mutable DevBuf<double> rx0, rx1, racc, ru;  // BVE segment recompute workspace
+  mutable DevBuf<double2> rs0, rs1;
+  bool checkpointed() const { return stride > 0; }
+  int segments() const { return stride > 0 ? (steps + stride - 1) / stride : 1; }
+  int held_steps() const { return stride > 0 ? std::min(stride, steps) : steps; }
+  // first step of the stored stage inputs (0 in full mode)
+  int held_k0() const { return stride > 0 ? seg * stride : 0; }
+  size_t stored_bytes() const {
+    return sizeof(double) * (w.size() + p.size() + final.size() + ckpt.size());
+  }
   const double* state_at(int step) const;  // step in [0, steps]
+  // stage inputs / streamfunctions of step k, stage s (k must be held)
+  const double* base_w(int k, int s, long long dim) const {
+    return w.get() + (static_cast<long long>(k - held_k0()) * stages + s) * dim;
+  }
+  const double* base_p(int k, int s, long long dim) const {
+    return p.get() + (static_cast<long long>(k - held_k0()) * stages + s) * dim;
+  }
 };
 
 class Problem {
@@ -60,8 +92,12 @@ class Problem {
   int total_steps() const { return d_.n_t * d_.spi; }
   cudaStream_t stream() const { return st_; }
 
-  // FWD nonlinear sweep from device x0, storing every RK4 stage input.
-  std::unique_ptr<Trajectory> linearize(const double* d_x0) const;
+  // FWD nonlinear sweep from device x0, storing every RK4 stage input (or,
+  // under kStoreCheckpoint / an auto fallback, checkpoints every `stride` steps).
+  std::unique_ptr<Trajectory> linearize(const double* d_x0, int stride = 0, int policy = kStoreAuto) const;
+  // Checkpoint mode: make the segment holding step k resident in tr.w / tr.p
+  // (recomputed from its checkpoint on the problem stream).
+  void hold_segment(const Trajectory& tr, int k) const;
   // Nonlinear forward of `steps` steps (device in/out), no storage.
   void forward(const double* d_x0, int steps, double* d_out) const;
 
@@ -156,6 +192,17 @@ class Problem {
   };
   std::vector<Lane> split_lanes(int v0, int gn) const;
   void join_lanes(const std::vector<Lane>& lanes) const;
+  void refork_lanes(const std::vector<Lane>& lanes) const;
+  // BVE NL forward of `steps` steps on u (in/out) with explicit workspace,
+  // storing stage inputs / streamfunctions when store_w != null.
+  struct NlWork {
+    double *x0, *x1, *acc;
+    double2 *s0, *s1;
+  };
+  void bve_nl(double* u, int steps, double* store_w, double* store_p, const NlWork& wk) const;
+  void linearize_ckpt(Trajectory& tr, const double* d_x0) const;
+  void fill_segment(const Trajectory& tr, int j) const;
+  void check_final(const Trajectory& tr) const;
   mutable std::vector<cudaStream_t> lane_st_;  // lanes 1.. of a sweep group (lane 0 runs on st_)
   mutable std::vector<cudaEvent_t> lane_ev_;
   mutable cudaEvent_t ev_fork_ = nullptr;

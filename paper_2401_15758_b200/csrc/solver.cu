@@ -801,7 +801,8 @@ struct Eval {
 };
 Eval evaluate_at(const Problem& p, const double* x, const double* z) {
   Eval e;
-  e.traj = p.linearize(x);
+  // proj/src/fourdvar.cpp:182: linearize(x0, total_steps, steps_per_interval)
+  e.traj = p.linearize(x, p.desc().spi, kStoreAuto);
   e.g.alloc(static_cast<size_t>(p.dim()));
   if (p.xspace()) e.gx.alloc(static_cast<size_t>(p.dim()));
   e.cost = p.evaluate(*e.traj, z, e.g.get(), nullptr, p.xspace() ? e.gx.get() : nullptr);
