@@ -18,6 +18,7 @@
 //                 Arakawa/Laplacian stencils with the stored base stage fields,
 //                 the RK4 (TLM/NL) or adjoint-RK4 (ADJ) update, and the forward
 //                 x-FFT of the next stage's Poisson input for the owned rows.
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -1259,6 +1260,19 @@ __global__ void scatter_obs_kernel(double* __restrict__ f, long long dim, const 
 }
 
 // ---------------------------------------------------------------- launchers --
+// 8-row stage CTAs below which a sweep lane counts as a small block. Measured
+// on B200 (tools/small_block.py, profiles/r2_small_blocks.md): the fused path
+// (8-row tiles + carry pass) beats the 2-row small-block path from 128 CTAs
+// per lane on every grid (512^2: 2 vectors, 256^2: 4, 128^2: 8), well below
+// the 296 CTA slots of one wave. SDV_FILL overrides (experiments).
+int bve_stage_fill() {
+  static const int f = [] {
+    const char* e = std::getenv("SDV_FILL");
+    return e ? std::max(1, std::atoi(e)) : 128;
+  }();
+  return f;
+}
+
 namespace {
 template <int N>
 struct Launch {
@@ -1269,7 +1283,7 @@ struct Launch {
   static constexpr int kSmallT = N >= 128 ? 2 : 8;
   using CS = Cfg<N, kSmallT>;
   static constexpr int kFill = 2 * 148;
-  static bool small_stage(int nvec) { return (N / C::kT) * nvec < kFill; }
+  static bool small_stage(int nvec) { return (N / C::kT) * nvec < bve_stage_fill(); }
   static bool small_col(int nvec) { return ((N / 2) / C::kCW) * nvec < kFill; }
   template <class K>
   static void smem_attr(K k, size_t bytes) {

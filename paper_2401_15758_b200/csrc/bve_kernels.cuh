@@ -72,6 +72,7 @@ void bve_stage(int n, int mode, const StageArgs& a, int nvec, cudaStream_t st, b
 // Whether a stage launch over nvec vectors takes the fused Poisson path
 // (8-row tiles; smaller blocks use 2-row tiles and the column pass).
 bool bve_fused_ok(int n, int nvec);
+int bve_stage_fill();  // 8-row stage CTAs per lane from which the fused path is taken
 // Small blocks on grids >= 256^2: the fused stage kernel with 2-row tiles as a
 // plain stage (in-place x-FFTs, stencil input staged up front), flags must
 // include kFlagRawIn | kFlagNoRecur; the column pass stays.

@@ -666,7 +666,10 @@ std::vector<Problem::Lane> Problem::split_lanes(int v0, int gn) const {
     const char* e = std::getenv("SDV_LANES");
     return e ? std::max(1, std::min(8, std::atoi(e))) : 2;
   }();
-  const int nl = std::min(nl_env, gn);
+  int nl = std::min(nl_env, gn);
+  // fused BVE blocks: every lane keeps at least bve_stage_fill() stage CTAs
+  // (narrow blocks run as one fused lane rather than two small-block lanes)
+  if (fused(gn)) nl = std::min(nl, std::max(1, (d_.n / 8) * gn / bve_stage_fill()));
   if (nl <= 1) {
     lanes.push_back(Lane{v0, gn, 0, st_});
     lanes.back().fz = fused(gn);
@@ -1000,7 +1003,11 @@ void Problem::gram_apply(const Trajectory& tr, const double* v, int s, double* h
   // Small blocks are launch-latency bound (thousands of short kernels per
   // sweep): capture the sweep once as a CUDA graph and replay it. The key is
   // every pointer the captured launches bake in.
-  if (s > 8 || std::getenv("SDV_NO_GRAPHS")) {
+  static const int graph_max = [] {
+    const char* e = std::getenv("SDV_GRAPH_MAX");
+    return e ? std::atoi(e) : 8;
+  }();
+  if (s > graph_max || std::getenv("SDV_NO_GRAPHS")) {
     run();
     return;
   }

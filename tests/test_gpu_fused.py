@@ -1,12 +1,13 @@
 """GPU parity of the fused Poisson path (stage kernels with tile-local
 y-recurrences + the tile-carry pass, bve_carry): the C3 hot path.
 
-A block is split into two sweep lanes of ceil(s/2) and floor(s/2) vectors
-(engine.cu split_lanes), and a lane takes the fused path only when its 8-row
-tiles fill >= 2 CTAs per SM: (n/8) * lane >= 296, i.e. lanes of >= 5 / 10 /
-19 / 37 vectors at 512^2 / 256^2 / 128^2 / 64^2, so blocks of >= 10 / 20 /
-38 / 74 vectors. Every case below is sized for that and ASSERTS the kernel
-path it took through the per-variant launch counters (sdv_path_counts). The
+A block takes the fused path when its 8-row tiles make >= 128 stage CTAs,
+(n/8) * s >= 128 (bve_stage_fill, measured on B200: tools/small_block.py):
+blocks of >= 2 / 4 / 8 / 16 vectors at 512^2 / 256^2 / 128^2 / 64^2. It runs as
+two concurrent sweep lanes of ceil(s/2) and floor(s/2) vectors once each lane
+keeps >= 128 CTAs, i.e. from twice those widths (engine.cu split_lanes). Every
+case below ASSERTS the kernel path it took through the per-variant launch
+counters (sdv_path_counts). The
 references are the column-pass path (SDV_NO_FUSE=1 SDV_NO_LITE=1: unfused
 8-row stage kernels + col_solve_kernel, also asserted) and the CPU oracle.
 Tolerances as test_gpu_parity (1e-10 relative for Hessian products and the
@@ -21,11 +22,12 @@ from test_gpu_parity import eig_rel, pair, rel
 
 pytestmark = pytest.mark.gpu
 
-# smallest block width that puts BOTH lanes on the fused path, per grid size
-FUSED_MIN = {64: 74, 128: 38, 256: 20, 512: 10}
+# smallest block width that takes the fused path (one lane), per grid size; two lanes from twice that
+FUSED_MIN = {64: 16, 128: 8, 256: 4, 512: 2}
 
-# (config, steps, spi, s): the minimum fused width and wider/odd widths
-CASES = [(3, 16, 8, 10), (3, 8, 4, 13), (2, 40, -1, 38), (2, 20, 10, 41), (4, 40, -1, 20), (4, 20, 10, 23)]
+# (config, steps, spi, s): the minimum fused widths (one lane, two lanes), odd and wider widths
+CASES = [(3, 8, 4, 2), (3, 8, 4, 5), (3, 16, 8, 10), (3, 8, 4, 13), (2, 20, 10, 8), (2, 40, -1, 38), (2, 20, 10, 41),
+         (4, 20, 10, 4), (4, 40, -1, 20), (4, 20, 10, 23)]
 
 
 def _env(column_path):
@@ -61,7 +63,8 @@ def fused_launches(took):
 
 
 def test_fused_min_width_table(sdv):
-    """The widths above are the boundary: one vector fewer leaves a lane off the fused path."""
+    """The widths above are the boundary: one vector fewer leaves the block off the fused path, twice the
+    width runs two fused lanes."""
     from paper_2401_15758_b200 import api, scenario
 
     for n, s in FUSED_MIN.items():
@@ -69,7 +72,7 @@ def test_fused_min_width_table(sdv):
                                       "spi": 1, "dt": 0.01 * 128 / n})
         sc = scenario.build(spec)
         tr = sc.problem.linearize(sc.problem.background)
-        for width, fused_lanes in ((s, 2), (s - 1, 1)):
+        for width, fused_lanes in ((2 * s, 2), (2 * s - 1, 1), (s, 1), (s - 1, 0)):
             V = api.gaussian_matrix(sc.problem.n, width, 3)
             before = sdv.path_counts()
             tr.misfit_apply(V)
