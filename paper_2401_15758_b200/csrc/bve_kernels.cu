@@ -124,8 +124,8 @@ template <int N>
 __global__ void __launch_bounds__(kThreads) row_fwd_kernel(const double* __restrict__ f, double2* __restrict__ s,
                                                            const double2* __restrict__ tw) {
   using C = Cfg<N>;
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   extern __shared__ double2 sm[];
   const int team = threadIdx.x / C::kTeam, t = threadIdx.x % C::kTeam;
   const int pair = blockIdx.x * C::kTeams + team;
@@ -147,8 +147,8 @@ template <int N>
 __global__ void __launch_bounds__(kThreads) row_inv_kernel(const double2* __restrict__ s, double* __restrict__ f,
                                                            const double2* __restrict__ tw) {
   using C = Cfg<N>;
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   extern __shared__ double2 sm[];
   const int team = threadIdx.x / C::kTeam, t = threadIdx.x % C::kTeam;
   const int pair = blockIdx.x * C::kTeams + team;
@@ -204,8 +204,8 @@ template <int N, int CW>
 __global__ void __launch_bounds__(CW*(N / 8)) col_kernel(double2* __restrict__ s, const double* __restrict__ sym,
                                                          const double2* __restrict__ tw) {
   extern __shared__ double2 sm[];
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   // Lanes interleave the kCW columns (team = column), so every warp-wide
   // global access covers kCW adjacent double2 of a few rows (coalesced); the
   // first forward pass reads global memory directly and the last inverse
@@ -266,8 +266,8 @@ __global__ void __launch_bounds__(256, N >= 512 ? 2 : 3)
     col_solve_kernel(double2* __restrict__ s, const double4* __restrict__ tab, const double* __restrict__ sym,
                      const double2* __restrict__ tw) {
   constexpr int CS = 8, SEG = 32, RPS = N / SEG;
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   if (blockIdx.x == gridDim.x - 1) {
     extern __shared__ double2 sm[];
     col_fft_body<N, 1>(s, sym, tw, sm, 0, 0, threadIdx.x, threadIdx.x < N / 8, blockIdx.y);
@@ -449,8 +449,8 @@ __global__ void __launch_bounds__(256, 2) carry_kernel(double2* __restrict__ s, 
                                                     const double4* __restrict__ tab) {
   constexpr int T = 8, Q = N / T, NPT = 8, QP = Q / NPT;
   static_assert(Q % NPT == 0, "carry_kernel: N / 8 tiles must split into 8 parts");
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x % 32, pt = threadIdx.x / 32;
   const long long v = blockIdx.y;
   if (blockIdx.x == gridDim.x - 1) {
@@ -565,7 +565,6 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
   const bool has_prev = MODE != kModeAdj || (p.flags & kFlagHasPrev);
   const bool finish = MODE == kModeAdj && (p.flags & kFlagFinish);
   const bool pf = !(p.flags & kFlagNoPrefetch);
-  pdl_trigger();
 
   // Prefetch what the later phases read, so it streams in under the inverse
   // FFT: the stencil's first base tile into L1 (shared by the whole tile,
@@ -1151,6 +1150,9 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
 
   }
 
+  // The successor (PDL launches only) may be scheduled from here: it starts
+  // while this launch runs its last phase and waits for its completion.
+  pdl_trigger();
   // Phase 4: forward x-FFT of the owned rows -> next row spectra.
   constexpr int kOwnPairs = T / 2;
   if constexpr (FUS) {
@@ -1241,8 +1243,8 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
 __global__ void gather_obs_kernel(const double* __restrict__ f, long long dim, const long long* __restrict__ idx,
                                   int n_obs, const double* __restrict__ w, double* __restrict__ y, long long m,
                                   int nvec) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (e >= static_cast<long long>(n_obs) * nvec) return;
   const int v = static_cast<int>(e / n_obs), k = static_cast<int>(e % n_obs);
@@ -1251,8 +1253,8 @@ __global__ void gather_obs_kernel(const double* __restrict__ f, long long dim, c
 __global__ void scatter_obs_kernel(double* __restrict__ f, long long dim, const long long* __restrict__ idx,
                                    int n_obs, const double* __restrict__ w, const double* __restrict__ y, long long m,
                                    int nvec) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (e >= static_cast<long long>(n_obs) * nvec) return;
   const int v = static_cast<int>(e / n_obs), k = static_cast<int>(e % n_obs);
@@ -1289,6 +1291,8 @@ struct Launch {
   static void smem_attr(K k, size_t bytes) {
     SDV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
   }
+  // PDL gate of this launch shape (common.cuh): off for one-vector 512^2 lanes
+  static void gate(int nvec) { pdl_gate() = !(N >= 512 && nvec == 1); }
   static void setup() {
     static const bool once = [] {  // thread-safe one-time kernel attributes (magic static)
       setup_once();
@@ -1307,16 +1311,19 @@ struct Launch {
   }
   static void row_fwd(const double* f, double2* s, int nvec, cudaStream_t st) {
     setup();
+    gate(nvec);
     dim3 g(ceil_div(N / 2, C::kTeams), nvec);
     launch_pdl(row_fwd_kernel<N>, g, kThreads, C::kRowSmem, st, f, s, twiddle_table(N));
   }
   static void row_inv(const double2* s, double* f, int nvec, cudaStream_t st) {
     setup();
+    gate(nvec);
     dim3 g(ceil_div(N / 2, C::kTeams), nvec);
     launch_pdl(row_inv_kernel<N>, g, kThreads, C::kRowSmem, st, s, f, twiddle_table(N));
   }
   static void col(double2* s, const double* sym, int nvec, cudaStream_t st) {
     setup();
+    gate(nvec);
     count_path(kPathBveColFft);
     if (small_col(nvec)) {
       launch_pdl(col_kernel<N, 1>, dim3(N / 2, nvec), C::kTeam, Cfg<N, 8, 1>::kColSmem, st, s, sym,
@@ -1330,6 +1337,7 @@ struct Launch {
   // singular) by the FFT column kernel on that one column.
   static void col_solve(double2* s, const double4* tab, const double* sym, int nvec, cudaStream_t st) {
     setup();
+    gate(nvec);
     // Small blocks (PCG / line-search sweeps, one vector): the solver's N/16+1
     // CTAs per vector would leave most SMs idle; the 1-column FFT kernel has
     // N/2 CTAs per vector.
@@ -1355,6 +1363,7 @@ struct Launch {
   static void stage_lite(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
     if constexpr (kLite) {
       setup();
+    gate(nvec);
       count_path(kPathBveStageLite);
       const dim3 g(N / kSmallT, nvec), b(kThreads);
       const bool tlm = mode == kModeTlm;
@@ -1377,6 +1386,7 @@ struct Launch {
   }
   static void stage_fused_impl(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
     setup();
+    gate(nvec);
     count_path(kPathBveStageFused);
     const dim3 g(N / 8, nvec), b(kThreads);
     const bool tlm = mode == kModeTlm;
@@ -1391,6 +1401,7 @@ struct Launch {
   static void carry(double2* s, const double2* lsum, double2* cc, double2* ce, const double4* tab, const double* sym,
                     int nvec, cudaStream_t st) {
     setup();
+    gate(nvec);
     if constexpr (N >= 64) {
       count_path(kPathBveCarry);
       launch_pdl(carry_kernel<N>, dim3(ceil_div(N / 2, 32) + 1, nvec), 256, 0, st, s, lsum, cc, ce, tab);
@@ -1422,6 +1433,7 @@ struct Launch {
   }
   static void stage(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
     setup();
+    gate(nvec);
     count_path(kPathBveStagePlain);
     if (small_stage(nvec)) stage_t<kSmallT>(mode, a, nvec, st);
     else stage_t<8>(mode, a, nvec, st);
