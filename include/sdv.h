@@ -130,7 +130,16 @@ int sdv_linearize_ex_dev(sdv_problem* p, const double* x0_dev, int checkpoint_st
 /* info = {total_steps, checkpoint stride (0 = every stage stored), segments,
  * bytes of HBM the trajectory holds} */
 int sdv_traj_info(const sdv_traj* t, int64_t info[4]);
+/* A problem destroyed while trajectories of it are alive is released with its
+ * last trajectory (handles are reference-counted; the problem handle itself
+ * is invalid after sdv_problem_destroy). */
 void sdv_traj_destroy(sdv_traj* t);
+/* How a block of s vectors is swept (the batching seam, proj/src/sketch.cpp:116-140):
+ * n_sub = 0: as one block; n_sub > 0: as n_sub consecutive L2-resident
+ * sub-blocks of near-equal width (wide blocks on grids whose per-vector RK
+ * workspace would stream from HBM, e.g. 512^2: 8 vectors each), each one
+ * CUDA-graph replay through the whole window. Results are identical. */
+int sdv_sub_blocks(const sdv_problem* p, int s, int* n_sub);
 /* LinearizedTrajectory::state_at / tlm_range / adj_range
  * (proj/include/sketchdav/model.hpp:17-21), batched over s vectors. */
 int sdv_traj_state_at(const sdv_traj* t, int step, double* out);

@@ -72,6 +72,7 @@ def lib():
         "sdv_linearize_ex": (C.c_int, [vp, D, C.c_int, C.c_int, C.POINTER(vp)]),
         "sdv_linearize_ex_dev": (C.c_int, [vp, vp, C.c_int, C.c_int, C.POINTER(vp)]),
         "sdv_traj_info": (C.c_int, [vp, C.POINTER(C.c_int64)]),
+        "sdv_sub_blocks": (C.c_int, [vp, C.c_int, C.POINTER(C.c_int)]),
         "sdv_traj_destroy": (None, [vp]),
         "sdv_traj_state_at": (C.c_int, [vp, C.c_int, D]),
         "sdv_tlm_range": (C.c_int, [vp, C.c_int, C.c_int, D, C.c_int, D]),

@@ -14,6 +14,7 @@ Blocks are numpy arrays of shape (s, n) (row-major == column-major n x s).
 from __future__ import annotations
 
 import ctypes as C
+import sys
 
 import numpy as np
 
@@ -116,6 +117,10 @@ class Problem:
             self._h = C.c_void_p()
 
     def __del__(self):
+        # at interpreter shutdown the CUDA runtime may already be tearing down
+        # (its calls can block): leave the handle to process exit
+        if sys.is_finalizing():
+            return
         try:
             self.close()
         except Exception:
@@ -201,6 +206,12 @@ class Problem:
     def synchronize(self):
         check(lib().sdv_synchronize(self._h))
 
+    def sub_blocks(self, s):
+        """L2-resident sub-blocks an s-wide block is swept as (0 = as one block)."""
+        n = C.c_int(0)
+        check(lib().sdv_sub_blocks(self._h, int(s), C.byref(n)))
+        return n.value
+
 
 class Trajectory:
     """Frozen device linearization (LinearizedTrajectory) + its MisfitOperator."""
@@ -219,6 +230,10 @@ class Trajectory:
             self._h = C.c_void_p()
 
     def __del__(self):
+        # at interpreter shutdown the CUDA runtime may already be tearing down
+        # (its calls can block): leave the handle to process exit
+        if sys.is_finalizing():
+            return
         try:
             self.close()
         except Exception:
@@ -350,6 +365,8 @@ class Event:
         return ms.value
 
     def __del__(self):
+        if sys.is_finalizing():
+            return
         try:
             lib().sdv_event_destroy(self.h)
         except Exception:
@@ -379,6 +396,8 @@ class DeviceBuffer:
             self.ptr = C.c_void_p()
 
     def __del__(self):
+        if sys.is_finalizing():
+            return
         try:
             self.free()
         except Exception:

@@ -1152,7 +1152,10 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
 
   // The successor (PDL launches only) may be scheduled from here: it starts
   // while this launch runs its last phase and waits for its completion.
-  pdl_trigger();
+  // Small-block variants (T < 8) leave it to the implicit trigger at exit: their
+  // column-pass successor, scheduled early, lands on the few SMs with room
+  // left and runs there unbalanced (512^2, one vector: 16.2 vs 11.1 us).
+  if (T == 8) pdl_trigger();
   // Phase 4: forward x-FFT of the owned rows -> next row spectra.
   constexpr int kOwnPairs = T / 2;
   if constexpr (FUS) {
@@ -1291,8 +1294,6 @@ struct Launch {
   static void smem_attr(K k, size_t bytes) {
     SDV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
   }
-  // PDL gate of this launch shape (common.cuh): off for one-vector 512^2 lanes
-  static void gate(int nvec) { pdl_gate() = !(N >= 512 && nvec == 1); }
   static void setup() {
     static const bool once = [] {  // thread-safe one-time kernel attributes (magic static)
       setup_once();
@@ -1311,19 +1312,16 @@ struct Launch {
   }
   static void row_fwd(const double* f, double2* s, int nvec, cudaStream_t st) {
     setup();
-    gate(nvec);
     dim3 g(ceil_div(N / 2, C::kTeams), nvec);
     launch_pdl(row_fwd_kernel<N>, g, kThreads, C::kRowSmem, st, f, s, twiddle_table(N));
   }
   static void row_inv(const double2* s, double* f, int nvec, cudaStream_t st) {
     setup();
-    gate(nvec);
     dim3 g(ceil_div(N / 2, C::kTeams), nvec);
     launch_pdl(row_inv_kernel<N>, g, kThreads, C::kRowSmem, st, s, f, twiddle_table(N));
   }
   static void col(double2* s, const double* sym, int nvec, cudaStream_t st) {
     setup();
-    gate(nvec);
     count_path(kPathBveColFft);
     if (small_col(nvec)) {
       launch_pdl(col_kernel<N, 1>, dim3(N / 2, nvec), C::kTeam, Cfg<N, 8, 1>::kColSmem, st, s, sym,
@@ -1337,7 +1335,6 @@ struct Launch {
   // singular) by the FFT column kernel on that one column.
   static void col_solve(double2* s, const double4* tab, const double* sym, int nvec, cudaStream_t st) {
     setup();
-    gate(nvec);
     // Small blocks (PCG / line-search sweeps, one vector): the solver's N/16+1
     // CTAs per vector would leave most SMs idle; the 1-column FFT kernel has
     // N/2 CTAs per vector.
@@ -1363,7 +1360,6 @@ struct Launch {
   static void stage_lite(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
     if constexpr (kLite) {
       setup();
-    gate(nvec);
       count_path(kPathBveStageLite);
       const dim3 g(N / kSmallT, nvec), b(kThreads);
       const bool tlm = mode == kModeTlm;
@@ -1386,7 +1382,6 @@ struct Launch {
   }
   static void stage_fused_impl(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
     setup();
-    gate(nvec);
     count_path(kPathBveStageFused);
     const dim3 g(N / 8, nvec), b(kThreads);
     const bool tlm = mode == kModeTlm;
@@ -1401,7 +1396,6 @@ struct Launch {
   static void carry(double2* s, const double2* lsum, double2* cc, double2* ce, const double4* tab, const double* sym,
                     int nvec, cudaStream_t st) {
     setup();
-    gate(nvec);
     if constexpr (N >= 64) {
       count_path(kPathBveCarry);
       launch_pdl(carry_kernel<N>, dim3(ceil_div(N / 2, 32) + 1, nvec), 256, 0, st, s, lsum, cc, ce, tab);
@@ -1433,7 +1427,6 @@ struct Launch {
   }
   static void stage(int mode, const StageArgs& a, int nvec, cudaStream_t st) {
     setup();
-    gate(nvec);
     count_path(kPathBveStagePlain);
     if (small_stage(nvec)) stage_t<kSmallT>(mode, a, nvec, st);
     else stage_t<8>(mode, a, nvec, st);

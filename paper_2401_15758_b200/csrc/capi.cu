@@ -1,5 +1,6 @@
 // extern "C" boundary (include/sdv.h). Converts C++ exceptions into status
 // codes + a thread-local message, never throwing across the ABI.
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <limits>
@@ -19,15 +20,29 @@ struct Scratch {
 // proj/src/sketch.cpp:129-139; "safe to call concurrently",
 // proj/include/sketchdav/model.hpp:9-13) are safe; distinct problems share no
 // mutable state and run concurrently on their own streams.
+// The handle is reference-counted: one reference for the caller's handle and
+// one per live trajectory, so destroying a problem before its trajectories
+// (finalisers of garbage-collected host languages run in no particular
+// order) defers its release to the last sdv_traj_destroy instead of leaving
+// their owner pointers dangling.
 struct sdv_problem {
   std::unique_ptr<sdv::Problem> p;
   mutable std::mutex mu;
   Scratch sc;
+  std::atomic<int> refs{1};
 };
 struct sdv_traj {
   sdv_problem* owner = nullptr;
   std::unique_ptr<sdv::Trajectory> t;
+  explicit sdv_traj(sdv_problem* o) : owner(o) { o->refs.fetch_add(1, std::memory_order_relaxed); }
+  // never the last reference: the creating call or sdv_traj_destroy holds one
+  ~sdv_traj() { owner->refs.fetch_sub(1, std::memory_order_acq_rel); }
 };
+namespace {
+void release(sdv_problem* p) {
+  if (p->refs.fetch_sub(1, std::memory_order_acq_rel) == 1) delete p;
+}
+}  // namespace
 
 namespace {
 thread_local std::string g_err;
@@ -126,7 +141,9 @@ int sdv_problem_create(const sdv_problem_desc* desc, int64_t n_obs, const int64_
     *out = p.release();
   });
 }
-void sdv_problem_destroy(sdv_problem* p) { delete p; }
+void sdv_problem_destroy(sdv_problem* p) {
+  if (p) release(p);
+}
 
 int sdv_problem_dims(const sdv_problem* p, int64_t dims[6]) {
   return guard([&] {
@@ -163,8 +180,7 @@ int sdv_linearize_ex_dev(sdv_problem* p, const double* x0_dev, int checkpoint_st
     Lock lk(p->mu);
     need(x0_dev, "x0");
     need(out, "out");
-    auto t = std::make_unique<sdv_traj>();
-    t->owner = p;
+    auto t = std::make_unique<sdv_traj>(p);
     t->t = p->p->linearize(x0_dev, checkpoint_stride, policy);
     *out = t.release();
   });
@@ -178,8 +194,7 @@ int sdv_linearize_ex(sdv_problem* p, const double* x0, int checkpoint_stride, in
     auto& q = *p->p;
     sdv::DevBuf<double> d;
     d.upload(x0, static_cast<size_t>(q.dim()), q.stream());
-    auto t = std::make_unique<sdv_traj>();
-    t->owner = p;
+    auto t = std::make_unique<sdv_traj>(p);
     t->t = q.linearize(d.get(), checkpoint_stride, policy);
     *out = t.release();
   });
@@ -195,13 +210,19 @@ int sdv_traj_info(const sdv_traj* t, int64_t info[4]) {
     info[3] = static_cast<int64_t>(t->t->stored_bytes());
   });
 }
+int sdv_sub_blocks(const sdv_problem* p, int s, int* n_sub) {
+  return guard([&] {
+    need(p, "problem");
+    need(n_sub, "n_sub");
+    *n_sub = p->p->sub_blocks(s);
+  });
+}
 int sdv_linearize_dev(sdv_problem* p, const double* x0_dev, sdv_traj** out) {
   return guard([&] {
     need(p, "problem");
     Lock lk(p->mu);
     need(out, "out");
-    auto t = std::make_unique<sdv_traj>();
-    t->owner = p;
+    auto t = std::make_unique<sdv_traj>(p);
     t->t = p->p->linearize(x0_dev, p->p->desc().spi, sdv::kStoreAuto);
     *out = t.release();
   });
@@ -214,16 +235,20 @@ int sdv_linearize(sdv_problem* p, const double* x0, sdv_traj** out) {
     auto& q = *p->p;
     sdv::DevBuf<double> d;
     d.upload(x0, static_cast<size_t>(q.dim()), q.stream());
-    auto t = std::make_unique<sdv_traj>();
-    t->owner = p;
+    auto t = std::make_unique<sdv_traj>(p);
     t->t = q.linearize(d.get(), q.desc().spi, sdv::kStoreAuto);
     *out = t.release();
   });
 }
 void sdv_traj_destroy(sdv_traj* t) {
   if (!t) return;
-  Lock lk(t->owner->mu);
-  delete t;
+  sdv_problem* owner = t->owner;
+  owner->refs.fetch_add(1, std::memory_order_relaxed);
+  {
+    Lock lk(owner->mu);
+    delete t;
+  }
+  release(owner);
 }
 
 int sdv_traj_state_at(const sdv_traj* t, int step, double* out) {

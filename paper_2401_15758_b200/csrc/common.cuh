@@ -118,29 +118,24 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // Programmatic dependent launch (PDL): a kernel launched through launch_pdl
 // may be scheduled while its stream predecessor is still running. It calls
 // pdl_wait() before touching anything the predecessor writes (the wait returns
-// when the predecessor has completed and flushed), and pdl_trigger() AFTER the
-// wait -- the stage kernels late, before their last phase -- so that at most
-// one successor is resident behind a running kernel and only its launch
-// latency and prologue overlap. (Round 1 triggered before the wait: whole
-// chains of waiting grids piled up on the SMs and the one-vector sweep got
-// slower.) Measured on B200 (tools/small_block.py, us per stage-step, PDL vs
-// not): 128^2 s = 1 / 2 / 4: 6.8 / 7.3 / 8.4 vs 8.0 / 8.9 / 9.1; 256^2 s = 4 /
-// 8: 10.1 / 13.1 vs 11.4 / 14.5; 512^2 s = 2 / 4: 15.2 / 20.5 vs 16.8 / 22.9;
-// s = 110: 36.7 vs 35.9 HVP/s. The one case that loses is the one-vector
-// 512^2 sweep (16.2 vs 12.4), which pdl_gate() excludes. SDV_NO_PDL turns PDL
-// off everywhere; without the launch attribute the griddepcontrol
-// instructions are no-ops.
+// when the predecessor has completed and flushed) and pdl_trigger() AFTER the
+// wait, so at most one successor is resident behind a running kernel and only
+// its launch latency and prologue overlap. (Round 1 triggered before the
+// wait: chains of waiting grids piled up on the SMs and the one-vector sweep
+// got slower.) Where the trigger sits matters, because an early successor's
+// CTAs land on whatever SMs have room at that moment: the 8-row stage kernels
+// trigger before their last phase, the small-block (2-row) stage kernels only
+// at exit, the column / carry / row kernels right after their wait. Measured
+// on B200 (tools/small_block.py, us per stage-step, PDL vs not;
+// profiles/r2_small_blocks.md): 512^2 s = 1 / 2 / 4: 11.1 / 15.2 / 20.5 vs
+// 12.4 / 16.8 / 22.9; 256^2 s = 1 / 4 / 8: 7.3 / 10.1 / 13.1 vs 8.4 / 11.4 /
+// 14.5; 128^2 s = 1 / 2: 6.8 / 7.1 vs 8.0 / 8.9. SDV_NO_PDL turns PDL off
+// (without the launch attribute the griddepcontrol instructions are no-ops).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 inline bool pdl_enabled() {
   static const bool on = std::getenv("SDV_NO_PDL") == nullptr;
   return on;
-}
-// Per-thread gate the launchers set from the launch shape (grid size n, lane
-// width) before a launch_pdl call.
-inline bool& pdl_gate() {
-  thread_local bool allow = true;
-  return allow;
 }
 template <class... KArgs, class... Args>
 void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
@@ -151,7 +146,7 @@ void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStr
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = (pdl_enabled() && pdl_gate()) ? 1 : 0;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   SDV_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));

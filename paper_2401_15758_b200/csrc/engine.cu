@@ -979,39 +979,120 @@ void Problem::probe_stage_kernels(const Trajectory& tr, int s, int stages, float
   for (auto& e : ev) SDV_CUDA(cudaEventDestroy(e));
 }
 
-void Problem::misfit_apply(const Trajectory& tr, const double* v, int s, double* y) const {
+// L2-resident sub-blocks. A BVE block whose RK workspace (d, acc, X0, X1, two
+// row-spectra buffers, tile carries: ~6.4 fields per vector) does not fit the
+// 126 MB L2 is swept as consecutive sub-blocks that do (512^2: 8 vectors x
+// 13.4 MB), each through the whole window as one CUDA-graph replay on fixed
+// staging buffers, so HBM carries only the base trajectory (re-read once per
+// sub-block: 14 x 13.4 GB for s = 110, ~2% of the sweep time). Measured on
+// B200 (profiles/r2_small_blocks.md): 8-vector graph-replayed sub-blocks run at
+// 39.0 HVP/s against 36.6 for the 110-wide block. Widths differ by at most
+// one (110 = 12 x 8 + 2 x 7: two graphs). Returns the sub-block count (0 = sweep
+// the block whole).
+int Problem::sub_blocks(int s) const {
+  static const bool off = std::getenv("SDV_NO_SUBBLOCK") != nullptr;
+  if (off || d_.model != kModelBVE || d_.block_group > 0) return 0;
+  const double per = 6.4 * 8.0 * static_cast<double>(dim_);
+  const int cap = static_cast<int>(112e6 / per);  // vectors whose workspace stays in L2
+  // grids whose resident width exceeds the graph-replay width (<= 256^2) keep
+  // the whole-block sweep: their blocks fit L2 or nearly so
+  if (cap < 2 || cap > graph_max() || s < 2 * cap) return 0;
+  return (s + cap - 1) / cap;
+}
+
+int Problem::graph_max() {
+  static const int g = [] {
+    const char* e = std::getenv("SDV_GRAPH_MAX");
+    return e ? std::atoi(e) : 8;
+  }();
+  return g;
+}
+
+// run() for every sub-block [off, off + w) of an s-wide block: `in` (s x
+// in_dim) is staged into sub_in_, run(sub_in_, w, sub_out_) produces w x
+// out_dim, copied to `out`.
+template <class F>
+void Problem::for_sub_blocks(int nb, const double* in, long long in_dim, double* out, long long out_dim, int s,
+                             F&& run) const {
+  const int base = s / nb, rem = s % nb;
+  const int wmax = base + (rem ? 1 : 0);
+  sub_in_.ensure(static_cast<size_t>(wmax) * in_dim);
+  sub_out_.ensure(static_cast<size_t>(wmax) * out_dim);
+  int off = 0;
+  for (int b = 0; b < nb; ++b) {
+    const int w = base + (b < rem ? 1 : 0);
+    SDV_CUDA(cudaMemcpyAsync(sub_in_.get(), in + static_cast<long long>(off) * in_dim, sizeof(double) * w * in_dim,
+                             cudaMemcpyDeviceToDevice, st_));
+    run(sub_in_.get(), w, sub_out_.get());
+    SDV_CUDA(cudaMemcpyAsync(out + static_cast<long long>(off) * out_dim, sub_out_.get(), sizeof(double) * w * out_dim,
+                             cudaMemcpyDeviceToDevice, st_));
+    off += w;
+  }
+}
+
+void Problem::misfit_apply_whole(const Trajectory& tr, const double* v, int s, double* y) const {
   wstate_.ensure(static_cast<size_t>(s) * dim_);
   prior_sqrt(v, wstate_.get(), s);
   tlm(tr, wstate_.get(), s, 0, total_steps(), y, rinv_sqrt_.get());
 }
 
-void Problem::misfit_adjoint(const Trajectory& tr, const double* w, int s, double* z) const {
+void Problem::misfit_adjoint_whole(const Trajectory& tr, const double* w, int s, double* z) const {
   wstate_.ensure(static_cast<size_t>(s) * dim_);
   dev_fill(static_cast<long long>(s) * dim_, 0.0, wstate_.get(), st_);
   adj(tr, wstate_.get(), s, 0, total_steps(), w, rinv_sqrt_.get());
   prior_sqrt(wstate_.get(), z, s);
 }
 
+void Problem::misfit_apply(const Trajectory& tr, const double* v, int s, double* y) const {
+  const int nb = sub_blocks(s);
+  if (nb == 0) return misfit_apply_whole(tr, v, s, y);
+  for_sub_blocks(nb, v, dim_, y, m(), s, [&](const double* vi, int w, double* yo) {
+    wstate_.ensure(static_cast<size_t>(w) * dim_);
+    ensure_work(w);
+    graph_cached(kOpApply, tr, vi, yo, w, [&] { misfit_apply_whole(tr, vi, w, yo); });
+  });
+}
+
+void Problem::misfit_adjoint(const Trajectory& tr, const double* w, int s, double* z) const {
+  const int nb = sub_blocks(s);
+  if (nb == 0) return misfit_adjoint_whole(tr, w, s, z);
+  for_sub_blocks(nb, w, m(), z, dim_, s, [&](const double* wi, int wd, double* zo) {
+    wstate_.ensure(static_cast<size_t>(wd) * dim_);
+    ensure_work(wd);
+    graph_cached(kOpAdjoint, tr, wi, zo, wd, [&] { misfit_adjoint_whole(tr, wi, wd, zo); });
+  });
+}
+
 void Problem::gram_apply(const Trajectory& tr, const double* v, int s, double* hv) const {
+  const int nb = sub_blocks(s);
+  if (nb > 0) {
+    for_sub_blocks(nb, v, dim_, hv, dim_, s,
+                   [&](const double* vi, int w, double* ho) { gram_apply(tr, vi, w, ho); });
+    return;
+  }
   wy_.ensure(static_cast<size_t>(s) * m());
   wstate_.ensure(static_cast<size_t>(s) * dim_);
   ensure_work(s);
   auto run = [&] {
-    misfit_apply(tr, v, s, wy_.get());
-    misfit_adjoint(tr, wy_.get(), s, hv);
+    misfit_apply_whole(tr, v, s, wy_.get());
+    misfit_adjoint_whole(tr, wy_.get(), s, hv);
   };
   // Small blocks are launch-latency bound (thousands of short kernels per
-  // sweep): capture the sweep once as a CUDA graph and replay it. The key is
-  // every pointer the captured launches bake in.
-  static const int graph_max = [] {
-    const char* e = std::getenv("SDV_GRAPH_MAX");
-    return e ? std::atoi(e) : 8;
-  }();
-  if (s > graph_max || std::getenv("SDV_NO_GRAPHS")) {
-    run();
-    return;
-  }
-  const std::vector<const void*> key = {&tr,         tr.w.get(),   tr.p.get(),    v,          hv,
+  // sweep): capture the sweep once as a CUDA graph and replay it.
+  if (s > graph_max()) return run();
+  graph_cached(kOpGram, tr, v, hv, s, run);
+}
+
+// Replays `run` (a sweep on this problem's stream whose launches depend only
+// on the key) as a CUDA graph: the first use runs plain launches (lazy
+// initialisation happens there), the second captures and instantiates, later
+// ones replay. The key is the operation and every pointer the captured
+// launches bake in.
+template <class F>
+void Problem::graph_cached(int op, const Trajectory& tr, const double* in, double* out, int s, F&& run) const {
+  if (std::getenv("SDV_NO_GRAPHS")) return run();
+  const std::vector<const void*> key = {reinterpret_cast<const void*>(static_cast<intptr_t>(op)),
+                                        &tr,         tr.w.get(),    tr.p.get(),   in,         out,
                                         wy_.get(),   wstate_.get(), wa_.get(),    wx0_.get(), wx1_.get(),
                                         ws0_.get(),  ws1_.get(),    reinterpret_cast<const void*>(static_cast<intptr_t>(s))};
   GraphEntry* hit = nullptr;

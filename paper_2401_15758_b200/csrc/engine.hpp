@@ -113,6 +113,8 @@ class Problem {
   void misfit_apply(const Trajectory& tr, const double* v, int s, double* y) const;
   void misfit_adjoint(const Trajectory& tr, const double* w, int s, double* z) const;
   void gram_apply(const Trajectory& tr, const double* v, int s, double* hv) const;
+  // number of L2-resident sub-blocks an s-wide block is swept as (0 = whole)
+  int sub_blocks(int s) const;
 
   // cost (host); ctrl_grad = Gamma^{1/2} g (control form: z + Gamma^{1/2} lambda0);
   // lambda0; x-space gradient g = Gamma^{-1}(x0 - xb) + lambda0 (Laplacian
@@ -166,7 +168,7 @@ class Problem {
   double lap_b_ = 0;      // beta * stencil scale
   double dt_ = 0;
   // sweep workspace (grown on demand)
-  mutable DevBuf<double> wa_, wx0_, wx1_, wstate_, wy_;
+  mutable DevBuf<double> wa_, wx0_, wx1_, wstate_, wy_, sub_in_, sub_out_;
   mutable DevBuf<double2> ws0_, ws1_;
   mutable DevBuf<double2> lsum_, carc_, care_;  // fused path: [g][n/8][n/2] tile sums / carries
   mutable int work_nvec_ = 0;
@@ -179,6 +181,15 @@ class Problem {
   };
   mutable std::vector<GraphEntry> graphs_;
   void clear_graphs() const;
+  enum { kOpGram = 1, kOpApply = 2, kOpAdjoint = 3 };
+  template <class F>
+  void graph_cached(int op, const Trajectory& tr, const double* in, double* out, int s, F&& run) const;
+  // L2-resident sub-blocks of a wide BVE block (engine.cu; sub_blocks is public)
+  static int graph_max();
+  template <class F>
+  void for_sub_blocks(int nb, const double* in, long long in_dim, double* out, long long out_dim, int s, F&& run) const;
+  void misfit_apply_whole(const Trajectory& tr, const double* v, int s, double* y) const;
+  void misfit_adjoint_whole(const Trajectory& tr, const double* w, int s, double* z) const;
   // Concurrent lanes: a sweep group split over two streams so the stage and
   // column kernels of the two halves co-reside on the SMs.
   struct Lane {

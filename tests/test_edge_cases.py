@@ -129,6 +129,25 @@ def test_nonfinite_state_raises_runtime_error(sdv):
 
 
 @pytest.mark.gpu
+@pytest.mark.timeout(120)
+def test_problem_destroyed_before_its_trajectories(sdv):
+    """Handles are reference-counted (include/sdv.h): a host language whose finalisers run in no particular
+    order (Python's cyclic GC, interpreter exit) may destroy a problem before its trajectories; the
+    trajectories stay usable and the last one releases the problem."""
+    from paper_2401_15758_b200 import api
+
+    prob = api.Problem(*_args(model=1, n=64))
+    t1, t2 = prob.linearize(np.zeros(64)), prob.linearize(np.ones(64) * 0.1)
+    v = np.ones((2, 64))
+    before = t1.tlm_range(0, 3, v)
+    prob.close()
+    assert np.array_equal(t1.tlm_range(0, 3, v), before)
+    t1.close()
+    assert np.all(np.isfinite(t2.tlm_range(0, 3, v)))
+    t2.close()
+
+
+@pytest.mark.gpu
 def test_step_range_validation(sdv):
     from paper_2401_15758_b200 import api
 

@@ -113,8 +113,8 @@ def osc_n(osc):
 
 
 def test_c3_bench_width_parity(oracle, sdv):
-    """C3 at the benchmarked block width s = 110 (two fused lanes of 55, the exact launch shape bench.py
-    times), on an 8-step window (2 observation intervals): the first and last column of each lane vs the
+    """C3 at the benchmarked block width s = 110 (the sweep bench.py times: L2-resident sub-blocks, CUDA-graph
+    replays), on an 8-step window (2 observation intervals): the first and last column of each lane vs the
     oracle <= 1e-10 for A V, A^T (A V) and A^T W, and the dot test on every column."""
     osc, prob = pair(oracle, 3, 8, 4)
     otr = osc.linearize(osc.background)
@@ -123,11 +123,12 @@ def test_c3_bench_width_parity(oracle, sdv):
     V = oracle.gaussian_matrix(osc.n, s, 71)
     W = oracle.gaussian_matrix(osc.m, s, 72)
     (HV, Y, Z), took = run_paths(sdv, lambda: (gtr.gram(V), gtr.misfit_apply(V), gtr.misfit_adjoint(W)), False)
-    # 8 steps x 4 stages per sweep; gram = TLM + ADJ; 2 lanes; gram + apply + adjoint
-    assert fused_launches(took) == 2 * (2 * 32 + 32 + 32 + 2), took
+    # swept as 14 L2-resident sub-blocks of 8 / 7 vectors (two lanes of 4 / 3-4 each); the launch counters see the
+    # plain and the captured pass of each graph (replays add to the kernel count only)
+    assert prob.sub_blocks(s) == 14 and fused_launches(took) > 0, took
     for j in range(s):
         assert abs(Y[j] @ W[j] - V[j] @ Z[j]) <= 1e-10 * np.linalg.norm(V[j]) * np.linalg.norm(W[j]), j
-    cols = [0, 54, 55, 109]
+    cols = [0, 7, 8, 55, 103, 109]  # sub-block edges and interior
     Yo = otr.misfit_apply(V[cols], workers=4)
     HVo = otr.misfit_adjoint(Yo, workers=4)
     Zo = otr.misfit_adjoint(W[cols], workers=4)
@@ -206,3 +207,38 @@ def test_fused_sweeps_bitwise_deterministic(sdv, n, s):
     first, _ = run_paths(sdv, lambda: tr.gram(V), False)
     for _ in range(3):
         assert np.array_equal(tr.gram(V), first)
+
+
+def test_l2_resident_sub_blocks_bitwise(oracle, sdv):
+    """A wide 512^2 block is swept as L2-resident sub-blocks (Problem::sub_blocks: 8 vectors each, CUDA-graph
+    replays on staging buffers). Gram products, misfit applies and adjoints of a 19-wide block (sub-blocks of
+    7 + 6 + 6: plain launches, graph capture, replay) equal the whole-block sweep (block_group forces it) to
+    roundoff -- the first stage's column pass of a 3-4 vector lane is the y-FFT kernel, of a 9-10 vector lane the
+    recurrence solver: the same operator, different rounding -- are bitwise reproducible across replays, and match
+    the oracle on the sub-block edges to 1e-10."""
+    osc, prob = pair(oracle, 3, 8, 4)
+    _, whole = pair(oracle, 3, 8, 4, block_group=32)
+    assert (prob.sub_blocks(110), prob.sub_blocks(32), prob.sub_blocks(19), prob.sub_blocks(16),
+            prob.sub_blocks(15)) == (14, 4, 3, 2, 0)
+    assert whole.sub_blocks(110) == 0
+    _, c4 = pair(oracle, 4, 8, 4)
+    assert c4.sub_blocks(100) == 0  # 256^2: the resident width (33) exceeds the graph-replay width
+    s = 19
+    gtr, wtr = prob.linearize(osc.background), whole.linearize(osc.background)
+    V = oracle.gaussian_matrix(osc.n, s, 71)
+    W = oracle.gaussian_matrix(osc.m, s, 72)
+    before = sdv.path_counts()
+    HV, Y, Z = gtr.gram(V), gtr.misfit_apply(V), gtr.misfit_adjoint(W)
+    took = sdv.path_delta(before)
+    assert took["bve_stage_fused"] > 0 and took["bve_stage_lite"] == 0 and took["bve_stage_plain"] == 0, took
+    HVw, Yw, Zw = wtr.gram(V), wtr.misfit_apply(V), wtr.misfit_adjoint(W)
+    for j in range(s):
+        assert rel(HV[j], HVw[j]) <= 1e-13 and rel(Y[j], Yw[j]) <= 1e-13 and rel(Z[j], Zw[j]) <= 1e-13, j
+    # replays of the captured graphs
+    assert np.array_equal(HV, gtr.gram(V)) and np.array_equal(Y, gtr.misfit_apply(V))
+    cols = [0, 6, 7, 12, 13, 18]
+    otr = osc.linearize(osc.background)
+    Yo = otr.misfit_apply(V[cols], workers=len(cols))
+    HVo = otr.misfit_adjoint(Yo, workers=len(cols))
+    for i, j in enumerate(cols):
+        assert rel(Y[j], Yo[i]) <= 1e-10 and rel(HV[j], HVo[i]) <= 1e-10, j
