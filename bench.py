@@ -502,8 +502,16 @@ def run_ours(args, world, rank, local):
             traffic = 0.5 * (t["dram_bytes_per_vector"] + ta["dram_bytes_per_vector"]) * g
             if "fp64_pipe_pct" in t and "fp64_pipe_pct" in ta:
                 fp64 = 0.5 * (t["fp64_pipe_pct"] + ta["fp64_pipe_pct"])
+    # the same kernel as the sweep launches it (4-vector lanes of an L2-resident
+    # sub-block): measured DRAM bytes per vector-stage, when profiled
+    traffic_sweep = None
+    if spec.model == api.MODEL_BVE and os.path.exists(tf) and prob.sub_blocks(s):
+        tsb = json.load(open(tf)).get("bve_stage_kernel_adj_subblock", {})
+        if tsb.get("grid") == spec.n:
+            traffic_sweep = {"dram_bytes_per_vector_stage": tsb["dram_bytes_per_vector"],
+                             "vectors_per_launch": tsb["vectors_per_launch"], "source": tsb["source"]}
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": traffic,
+            "traffic": traffic, "traffic_sweep_shape": traffic_sweep,
             # measured DRAM bytes (ncu) over the live launch time: how close the
             # kernel's actual data movement runs to the HBM peak
             "traffic_GBs": (traffic / (dur / 1000.0) / 1e9) if traffic else None,
