@@ -242,3 +242,31 @@ def test_l2_resident_sub_blocks_bitwise(oracle, sdv):
     HVo = otr.misfit_adjoint(Yo, workers=len(cols))
     for i, j in enumerate(cols):
         assert rel(Y[j], Yo[i]) <= 1e-10 and rel(HV[j], HVo[i]) <= 1e-10, j
+
+
+@pytest.mark.parametrize("cfg,s", [(3, 16), (4, 10)])
+def test_full_window_properties_at_baseline_size(sdv, cfg, s):
+    """BASELINE.json's full sizes (C3: 512^2, 800 RK4 steps, swept as L2-resident sub-blocks; C4: 256^2, 400
+    steps, its adaptive sketch's block of 10), where the oracle takes minutes per column: size-independent
+    properties instead -- the dot test <A v, w> = <v, A^T w> on every column, linearity of the block sweep
+    in its columns, H = A^T A symmetric and positive (v_i^T H v_j = v_j^T H v_i, v^T H v = |A v|^2), and
+    bitwise reproducibility. (tools/full_window_parity.py runs the oracle itself on a few columns;
+    profiles/r2_parity.md has its result.)"""
+    from paper_2401_15758_b200 import api, scenario
+
+    sc = scenario.build(cfg)
+    prob = sc.problem
+    tr = prob.linearize(prob.background)
+    V = api.gaussian_matrix(prob.n, s, 81)
+    W = api.gaussian_matrix(prob.m, s, 82)
+    V[2] = 0.5 * V[0] - 2.0 * V[1]  # a column that is a combination of two others
+    Y, Z, HV = tr.misfit_apply(V), tr.misfit_adjoint(W), tr.gram(V)
+    nv, nw = np.linalg.norm(V, axis=1), np.linalg.norm(W, axis=1)
+    for j in range(s):
+        assert abs(Y[j] @ W[j] - V[j] @ Z[j]) <= 1e-10 * nv[j] * nw[j], j
+        assert abs(V[j] @ HV[j] - Y[j] @ Y[j]) <= 1e-10 * (Y[j] @ Y[j]), j
+    assert rel(Y[2], 0.5 * Y[0] - 2.0 * Y[1]) <= 1e-11
+    assert rel(HV[2], 0.5 * HV[0] - 2.0 * HV[1]) <= 1e-11
+    G = V @ HV.T
+    assert np.max(np.abs(G - G.T)) <= 1e-10 * np.max(np.abs(G))
+    assert np.array_equal(tr.gram(V), HV)
