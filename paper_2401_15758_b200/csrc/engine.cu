@@ -1094,7 +1094,10 @@ void Problem::graph_cached(int op, const Trajectory& tr, const double* in, doubl
   const std::vector<const void*> key = {reinterpret_cast<const void*>(static_cast<intptr_t>(op)),
                                         &tr,         tr.w.get(),    tr.p.get(),   in,         out,
                                         wy_.get(),   wstate_.get(), wa_.get(),    wx0_.get(), wx1_.get(),
-                                        ws0_.get(),  ws1_.get(),    reinterpret_cast<const void*>(static_cast<intptr_t>(s))};
+                                        ws0_.get(),  ws1_.get(),    reinterpret_cast<const void*>(static_cast<intptr_t>(s)),
+                                        // the sweep structure the launches follow
+                                        reinterpret_cast<const void*>(static_cast<intptr_t>(tr.steps)),
+                                        reinterpret_cast<const void*>(static_cast<intptr_t>(tr.stride))};
   GraphEntry* hit = nullptr;
   for (auto& g : graphs_)
     if (g.key == key) hit = &g;

@@ -3,6 +3,7 @@
 // linesearch}.cpp (file:line at each function). The n x l contractions
 // (Householder QR, Gram, tall x small products, row triangular solves) run on
 // the device; the l x l SVD / Cholesky / pseudo-inverse on the host.
+#include <future>
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
@@ -116,7 +117,27 @@ void orthogonalize_block(double* y, int ly, const double* q, int lq, long long n
     }
 }
 
+// The host RNG (bit-exact mt19937_64 + Box-Muller, proj/src/rng.cpp:9-48) needs
+// ~1.2 s for C3's 262144 x 110 test block, during which the GPU would idle.
+// gn_solve therefore has the NEXT iteration's block generated on a worker
+// thread while the GPU runs the current iteration's PCG; gaussian_dev picks
+// it up when (n, l, seed) match and generates inline otherwise.
+struct GaussPrefetch {
+  long long n = 0, l = 0;
+  uint64_t seed = 0;
+  std::future<std::vector<double>> fut;
+  void start(long long n_, long long l_, uint64_t seed_) {
+    n = n_;
+    l = l_;
+    seed = seed_;
+    fut = std::async(std::launch::async, [n_, l_, seed_] { return gaussian_matrix(n_, l_, seed_); });
+  }
+};
+thread_local GaussPrefetch* tl_gauss = nullptr;
+
 DevBuf<double> gaussian_dev(long long n, long long l, uint64_t seed, cudaStream_t st) {
+  if (tl_gauss && tl_gauss->fut.valid() && tl_gauss->n == n && tl_gauss->l == l && tl_gauss->seed == seed)
+    return to_dev(tl_gauss->fut.get(), st);
   return to_dev(gaussian_matrix(n, l, seed), st);
 }
 DevBuf<double> append_dev(const DevBuf<double>& a, long long la, const double* b, long long lb, long long n,
@@ -859,6 +880,11 @@ GNResult gn_solve(const Problem& p, const GNConfig& cfg) {
   sc0.eps_reuse = cfg.eps_reuse;
   DevBuf<double> rhs(static_cast<size_t>(n)), dxt(static_cast<size_t>(n)), dx(static_cast<size_t>(n)),
       tx(static_cast<size_t>(n)), tz(static_cast<size_t>(n));
+  GaussPrefetch gauss;
+  struct GaussScope {
+    explicit GaussScope(GaussPrefetch* g) { tl_gauss = g; }
+    ~GaussScope() { tl_gauss = nullptr; }
+  } gauss_scope(&gauss);
   for (int k = 0; k < cfg.max_gn_iters; ++k) {
     const double gnorm = inf_norm(ev.conv(), n, st);
     if (gnorm / g0 < cfg.grad_tol) {
@@ -913,6 +939,12 @@ GNResult gn_solve(const Problem& p, const GNConfig& cfg) {
       if (!rep.kappa.empty()) log.rec[9] = rep.kappa.back();
       if (!rep.tolerance_met) warn("gn_solve: adaptive sketch hit its rank cap at GN iteration " + std::to_string(k));
     }
+    // next iteration's Gaussian test block (the non-adaptive sketches draw
+    // n x rank with seed mix_seed(seed, kIterSketchStream + k + 1)), generated
+    // while the GPU solves this iteration's system; only when it is large
+    if (mode != 3 && mode != 4 && mode != 5 && !adaptive && !lanczos && sc0.method >= 0 && sc0.method <= 2 &&
+        k + 1 < cfg.max_gn_iters && static_cast<double>(n) * sc0.rank >= 4e6 && !std::getenv("SDV_NO_GAUSS_PREFETCH"))
+      gauss.start(n, sc0.rank, mix_seed(cfg.seed, kIterSketchStream + k + 1));
     if (mode == 0) {
       woodbury_apply(*held, ev.g.get(), dxt.get(), n, st);
       dev_axpby(n, -1.0, dxt.get(), 0.0, dxt.get(), st);
