@@ -852,17 +852,25 @@ __global__ void __launch_bounds__(kThreads, 2) stage_kernel(StageArgs p) {
         ldg(G, q + 1, wg[s2]);
         if (MODE == kModeTlm && pass == 1 && q + 1 < RPG) rkload(q + 1);
         double kk[2];
+        {
+          // rows -1, 0, +1 of the field and base windows (ring slots renamed)
+          const double Wr[3][4] = {{ws[s0][0], ws[s0][1], ws[s0][2], ws[s0][3]},
+                                   {ws[s1][0], ws[s1][1], ws[s1][2], ws[s1][3]},
+                                   {ws[s2][0], ws[s2][1], ws[s2][2], ws[s2][3]}};
+          const double Br[3][4] = {{wg[s0][0], wg[s0][1], wg[s0][2], wg[s0][3]},
+                                   {wg[s1][0], wg[s1][1], wg[s1][2], wg[s1][3]},
+                                   {wg[s2][0], wg[s2][1], wg[s2][2], wg[s2][3]}};
+          double jj[2];  // 12 h^2 J(base, field) at the two columns
+          arakawa12_pair(Br, Wr, jj);
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const double W[3][3] = {{ws[s0][c], ws[s0][c + 1], ws[s0][c + 2]},
-                                  {ws[s1][c], ws[s1][c + 1], ws[s1][c + 2]},
-                                  {ws[s2][c], ws[s2][c + 1], ws[s2][c + 2]}};
-          const double B[3][3] = {{wg[s0][c], wg[s0][c + 1], wg[s0][c + 2]},
-                                  {wg[s1][c], wg[s1][c + 1], wg[s1][c + 2]},
-                                  {wg[s2][c], wg[s2][c + 1], wg[s2][c + 2]}};
-          if (MODE == kModeAdj) kk[c] = pass == 0 ? fma(-arakawa12(B, W), js, nls * lap5(W)) : -arakawa12(W, B) * js;
-          else if (pass == 0) kk[c] = fma(arakawa12(B, W), js, nls * lap5(W));
-          else kk[c] = (c ? rc[q].y : rc[q].x) + arakawa12(W, B) * js;
+          for (int c = 0; c < 2; ++c) {
+            const double lap = Wr[1][c] + Wr[1][c + 2] + Wr[0][c + 1] + Wr[2][c + 1] - 4.0 * Wr[1][c + 1];
+            // TLM A: J(psi_b, X) + nu Lap X;  B: + J(P, omega_b) = - J(omega_b, P)
+            // ADJ A: -J(psi_b, a) + nu Lap a;  B: -J(a, omega_b) = + J(omega_b, a)
+            if (MODE == kModeAdj) kk[c] = pass == 0 ? fma(-jj[c], js, nls * lap) : jj[c] * js;
+            else if (pass == 0) kk[c] = fma(jj[c], js, nls * lap);
+            else kk[c] = fma(-jj[c], js, c ? rc[q].y : rc[q].x);
+          }
         }
         if (MODE == kModeAdj) {
           // A: q_out = -J(psi_b, a) + nu Lap a (non-Poisson part of mu);

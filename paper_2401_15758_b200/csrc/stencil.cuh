@@ -17,4 +17,34 @@ __device__ __forceinline__ double lap5(const double o[3][3]) {
   return o[1][0] + o[1][2] + o[0][1] + o[2][1] - 4.0 * o[1][1];
 }
 
+
+// 12 h^2 J(a, b) at two adjacent points from 3x4 windows (rows -1, 0, +1; the
+// points' 3x3 neighbourhoods are columns 0..2 and 1..3), for a BASE field a
+// and a per-vector field b. The Arakawa Jacobian is bilinear, so for a fixed a
+// it is the 8-point stencil sum_k c_k(a) b_k (the centre coefficient is 0):
+//   north/south: +-(a_x at this row + a_x at that row), a_x = a(.,+1) - a(.,-1)
+//   east/west:   -+(a_y at this column + a_y at that column), a_y = a(+1,.) - a(-1,.)
+//   corners:     differences of the two edge neighbours next to the corner.
+// The column differences a_y and their pair sums are shared by the two
+// points: 21.5 fp64 instructions per point instead of arakawa12's 24. Same
+// operator (antisymmetric in (a, b): J(b, a) = -J(a, b)); roundoff differs.
+__device__ __forceinline__ void arakawa12_pair(const double a[3][4], const double b[3][4], double out[2]) {
+  const double dy0 = a[2][0] - a[0][0], dy1 = a[2][1] - a[0][1], dy2 = a[2][2] - a[0][2], dy3 = a[2][3] - a[0][3];
+  const double sy[3] = {dy0 + dy1, dy1 + dy2, dy2 + dy3};
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const double dx0 = a[0][p + 2] - a[0][p], dx1 = a[1][p + 2] - a[1][p], dx2 = a[2][p + 2] - a[2][p];
+    const double cn = dx1 + dx2, cs = dx1 + dx0;  // b(+1, 0), -b(-1, 0)
+    double r0 = cn * b[2][p + 1];
+    double r1 = sy[p] * b[1][p];                   // b(0, -1)
+    r0 = fma(-cs, b[0][p + 1], r0);
+    r1 = fma(-sy[p + 1], b[1][p + 2], r1);        // b(0, +1)
+    r0 = fma(a[1][p + 2] - a[2][p + 1], b[2][p + 2], r0);
+    r1 = fma(a[0][p + 1] - a[1][p + 2], b[0][p + 2], r1);
+    r0 = fma(a[2][p + 1] - a[1][p], b[2][p], r0);
+    r1 = fma(a[1][p] - a[0][p + 1], b[0][p], r1);
+    out[p] = r0 + r1;
+  }
+}
+
 }  // namespace sdv
