@@ -41,8 +41,11 @@ __device__ __forceinline__ void arakawa12_pair(const double a[3][4], const doubl
     r1 = fma(-sy[p + 1], b[1][p + 2], r1);        // b(0, +1)
     r0 = fma(a[1][p + 2] - a[2][p + 1], b[2][p + 2], r0);
     r1 = fma(a[0][p + 1] - a[1][p + 2], b[0][p + 2], r1);
-    r0 = fma(a[2][p + 1] - a[1][p], b[2][p], r0);
-    r1 = fma(a[1][p] - a[0][p + 1], b[0][p], r1);
+    // (written as minus the opposite corner's difference of the diagonal
+    // neighbour, so the unrolled row sweep reuses it: point (x, y)'s
+    // north-east coefficient is minus point (x+1, y+1)'s south-west one)
+    r0 = fma(-(a[1][p] - a[2][p + 1]), b[2][p], r0);
+    r1 = fma(-(a[0][p + 1] - a[1][p]), b[0][p], r1);
     out[p] = r0 + r1;
   }
 }
