@@ -26,7 +26,10 @@ __device__ __forceinline__ double lap5(const double o[3][3]) {
 //   east/west:   -+(a_y at this column + a_y at that column), a_y = a(+1,.) - a(-1,.)
 //   corners:     differences of the two edge neighbours next to the corner.
 // The column differences a_y and their pair sums are shared by the two
-// points: 21.5 fp64 instructions per point instead of arakawa12's 24. Same
+// points. ptxas finds most of this sharing in two inlined arakawa12 calls
+// too (the instruction count falls ~1%), but this form keeps fewer values
+// live: spills 24-120 -> 4-20 B per thread in the fused TLM stage kernels,
+// their launches 2.4% faster (profiles/r2s4_ncu_stage_streaming.md). Same
 // operator (antisymmetric in (a, b): J(b, a) = -J(a, b)); roundoff differs.
 __device__ __forceinline__ void arakawa12_pair(const double a[3][4], const double b[3][4], double out[2]) {
   const double dy0 = a[2][0] - a[0][0], dy1 = a[2][1] - a[0][1], dy2 = a[2][2] - a[0][2], dy3 = a[2][3] - a[0][3];
